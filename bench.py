@@ -1,0 +1,325 @@
+#!/usr/bin/env python
+"""bench.py -- Rasterized SMoE fit iterations/s (and render Mpix/s) on B200.
+
+Metric (BASELINE.json): "SMoE fit iterations/s and render Mpix/s at 1/2/4/8
+B200 (% of roofline)".  One bench step = one fit iteration of the whole hot
+path (§8(a) a1-a8: preprocess, binning, forward, loss, backward, Adam) over
+the configured synthetic workload; the render (a9) is timed separately and
+reported under "render".  Default workload: BASELINE.json config 2 (768x512
+RGB Kodak-shaped synthetic image, 10k kernels, linear experts; the metric's
+configuration).  N > 1 (torchrun): tile-row bands per rank, NCCL all-reduce
+of the gradients every step (paper_2510_05814_b200/dist.py).
+
+Timing: W warm-up steps; then K steps, each bracketed by CUDA events on the
+launch stream with an L2 flush (256 MB write) between steps outside the
+events; barrier + synchronize on both sides; max over ranks.  The library's
+own event pairs (smoe_profile_*) time every kernel inside the same region.
+
+--impl reference: the CPU oracle (oracle/), as it stands, on the host, on a
+bounded sample of the same workload per step (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# Algorithmic FP32 lane-op counts of the raster (from SURVEY
+# §8(d)): per tested (pixel, kernel) pair 7 (dx, dy, u, v x2, d^2 x2); per
+# pair inside the ellipse (2 + C + 2 C o) forward + (12 + 2 C + 4 C o) backward.
+def ops_per_unit(C, order):
+    return 7, (2 + C + 2 * C * order) + (12 + 2 * C + 4 * C * order)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "50"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = [l.strip().split(", ") for l in open(self.f.name) if l.strip()]
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if len(r) >= 9]
+        mx = [float(r[2]) for r in rows if len(r) >= 9]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            for n, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def rank_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def cpu_oracle_sample(target, pool, rows):
+    """Time the CPU oracle's loss+gradient on image rows [r0, r1) (dense over
+    all kernels, fp64, one thread) plus its Adam step.  Returns (seconds for
+    the rows, seconds for Adam)."""
+    import numpy as np
+    import oracle as O
+    op = O.Params.from_any(pool)
+    t = target.astype(np.float64)
+    t0 = time.perf_counter()
+    lg = O.loss_grad(op, t, rows=rows)
+    t1 = time.perf_counter()
+    opt = O.Adam(op.K, op.Pk)
+    opt.step(op, lg.grad, O.LR())
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1
+
+
+def run_reference(args):
+    rank, world, _ = rank_env()
+    if rank != 0:
+        return 0
+    from paper_2510_05814_b200 import synth
+    cfg = synth.CONFIGS[args.config]
+    target, _, pool = synth.workload(args.config)
+    H = cfg["H"]
+    rows_per_step = 1
+    times = []
+    for i in range(args.warmup + args.steps):
+        r0 = (i * 97) % (H - rows_per_step + 1)
+        tg, ta = cpu_oracle_sample(target, pool, (r0, r0 + rows_per_step))
+        if i >= args.warmup:
+            times.append((tg, ta))
+    tg = sum(t[0] for t in times) / len(times)
+    ta = sum(t[1] for t in times) / len(times)
+    sec_per_iter = tg * H / rows_per_step + ta
+    value = 1.0 / sec_per_iter
+    sample = (f"per step: dense fp64 loss+gradient of {rows_per_step} image row (of {H}) over all "
+              f"{cfg['K']} kernels + one full Adam step; it/s = 1/(H/rows * t_rows + t_adam)")
+    out = {
+        "impl": "reference", "metric": "SMoE fit iterations/s", "value": value, "unit": "it/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec_per_iter * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args.config, world),
+        "cpu_baseline": {"value": value, "unit": "it/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+    return 0
+
+
+def config_dict(name, world):
+    from paper_2510_05814_b200 import synth
+    c = synth.CONFIGS[name]
+    return {"workload": f"config{c['cfg']}-{name}", "H": c["H"], "W": c["W"], "C": c["C"], "K": c["K"],
+            "expert_order": c["order"], "fit_iterations": c["iters"],
+            "parallelism": f"tile-row bands x{world}" if world > 1 else "single GPU",
+            "l2": "flushed between timed steps (256 MB write)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="kodak", choices=["tiny", "kodak", "div2k", "denoise", "8k"])
+    ap.add_argument("--cpu-rows", type=int, default=64, help="image rows of the cpu_baseline sample")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-flush", action="store_true")
+    args = ap.parse_args()
+    assert args.warmup >= 3, "at least 3 warm-up steps"
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2510_05814_b200 import smoe, synth
+    from paper_2510_05814_b200.dist import BandedFit
+
+    rank, world, local = rank_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = synth.CONFIGS[args.config]
+    C, H, W, K, order = cfg["C"], cfg["H"], cfg["W"], cfg["K"], cfg["order"]
+    target, _, pool = synth.workload(args.config)
+    dev = torch.device("cuda", local)
+    tgt = torch.as_tensor(target).to(dev)
+    params = smoe.Params.from_numpy(pool, dev)
+    h = smoe.SMoE(K, H, W, C, order, device=local)
+    fit = BandedFit(h, rank, world) if world > 1 else None
+    T_total = args.warmup + args.steps
+
+    def step(t):
+        lr = smoe.LR.paper(t, T_total)
+        if fit is None:
+            h.step(params, tgt, lr, stats=False)
+        else:
+            fit.step(params, tgt, lr)
+
+    flush = None if args.no_flush else torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    st0 = h.step(params.clone(), tgt, smoe.LR(0, 0, 0, 0, 0), stats=True)   # calibrate capacity
+    h.reset_adam()
+    for t in range(args.warmup):
+        step(t)
+    h.sync()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    h.profile_begin(args.steps * 8 + 64)
+    launches0 = h.launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    for i in range(args.steps):
+        if flush is not None:
+            flush.zero_()
+        ev[i][0].record()
+        step(args.warmup + i)
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = h.launch_count() - launches0
+    ktimes, (tested, hits) = h.profile_end()
+    clk = clocks.stop()
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    tms = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tms, op=dist.ReduceOp.MAX)
+    total_ms = float(tms.item())
+    st = h.sync()
+    ms_step = total_ms / args.steps
+    value = 1e3 / ms_step   # whole-image fit iterations per second (all ranks together)
+
+    # roofline of the dominant kernel (raster: FP32 pipe)
+    peaks, peak_kind = load_peaks()
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    dom = max(ktimes.items(), key=lambda kv: kv[1][0])
+    dom_name, (dom_ms, dom_n) = dom
+    a_t, a_h = ops_per_unit(C, order)
+    roof = None
+    rast = ktimes.get("k_raster<train>")
+    if rast:
+        r_ms, r_n = rast
+        ops = (a_t * tested + a_h * hits) / r_n
+        achieved = ops / (r_ms / r_n * 1e-3) / 1e12
+        peak = 148 * 128 * sm_mhz * 1e6 / 1e12
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_raster_traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get(f"{args.config}", {}).get("dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        roof = {"bound": "alu", "kernel": "k_raster<train>", "achieved": achieved, "peak": peak,
+                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                "ops_note": f"FP32 lane-ops (FMA=1): {a_t}/tested pair + {a_h}/hit pair; peak = 148 SM x 128 "
+                            f"lanes x {sm_mhz:.0f} MHz ({peak_kind} sm_max_mhz)",
+                "tested_pairs_per_launch": tested / r_n, "hit_pairs_per_launch": hits / r_n,
+                "avg_ms": r_ms / r_n, "share_of_step": r_ms / total_ms if world == 1 else None}
+
+    # render (a9): plain reconstruction and the config's SR factor
+    render = {}
+    if rank == 0:
+        sr = cfg.get("sr", 1)
+        for s in sorted({1, sr}):
+            oH, oW = H * s, W * s
+            out = torch.empty((C, oH, oW), dtype=torch.float32, device=dev)
+            h.render(params, oH, oW, out)
+            torch.cuda.synchronize()
+            reps = 20
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            rt = 0.0
+            for _ in range(reps):
+                if flush is not None:
+                    flush.zero_()
+                e0.record()
+                h.render(params, oH, oW, out)
+                e1.record()
+                torch.cuda.synchronize()
+                rt += e0.elapsed_time(e1)
+            h.sync()
+            render[f"x{s}"] = {"mpix_s": oH * oW * reps / (rt * 1e-3) / 1e6, "ms": rt / reps, "out": [oH, oW]}
+
+    # e2e through the public API: pinned host target H2D + step + stats D2H
+    e2e = None
+    if not args.no_e2e and world == 1:
+        host_t = torch.as_tensor(target).pin_memory()
+        n_e2e = min(args.steps, 200)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i in range(n_e2e):
+            h.step(params, host_t, smoe.LR.paper(T_total, T_total), stats=True)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        e2e = {"value": n_e2e / dt, "unit": "it/s", "h2d_bytes_per_step": int(target.nbytes),
+               "d2h_bytes_per_step": 104, "steps": n_e2e}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rows = min(args.cpu_rows, H)
+        r0 = (H - rows) // 2
+        tg, ta = cpu_oracle_sample(target, pool, (r0, r0 + rows))
+        cpu = {"value": 1.0 / (tg * H / rows + ta), "unit": "it/s", "cores": 1, "kind": "oracle",
+               "sample": f"dense fp64 loss+gradient on image rows {r0}-{r0 + rows} of {H} ({rows * W} px x "
+                         f"{K} kernels, {tg:.1f} s) + full Adam ({ta:.3f} s), extrapolated to one iteration"}
+
+    if rank == 0:
+        out = {
+            "metric": "SMoE fit iterations/s", "value": value, "unit": "it/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config_dict(args.config, world),
+            "render": render, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clk,
+            "kernel_ms_per_step": {k: v[0] / args.steps for k, v in ktimes.items()},
+            "fit_stats": {"pairs": st.pairs, "avg_kernels_per_block": st.pairs / max(st.n_tiles, 1),
+                          "loss": st.loss, "psnr_db": st.psnr_db, "initial_psnr_db": st0.psnr_db},
+        }
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,210 @@
+/*
+ * smoe.h -- C ABI of the B200-native Rasterized SMoE hot path.
+ *
+ * Method: Rasterized Steered Mixture-of-Experts regression, arxiv 2510.05814
+ * (citations: P:n = PAPER.md line n; S:n = SPEC.md line n; Q-numbers are the
+ * readings listed in DESIGN.md).  A pixel x of an H x W x C image is
+ *
+ *     y(x) = sum_{j in K_n} m_j(x) w_j(x),                  Eq. (5)
+ *     w_j(x) = pi_j K_j(x) / sum_{i in K_n} pi_i K_i(x),     Eq. (4)
+ *     K_j(x) = exp(-1/2 (x-mu_j)^T Sigma_j^-1 (x-mu_j)),     Eq. (3)
+ *
+ * with Sigma_j = L_j L_j^T (Cholesky), pi_j = exp(log_pi_j), experts
+ * m_j(x) = m_j (constant) or m_j + W_j (x - mu_j) (linear), each kernel
+ * truncated at its 99% confidence ellipse d^2 <= R2 = 2 ln 100 (
+ * Q1-Q3) and binned into 16x16 blocks through the square box whose side is
+ * the major axis of that ellipse.  Pixel (row i, col j) is
+ * centred at (j, i); a pixel with no contributing kernel renders 0 (Q7).
+ *
+ * Every entry point returns a smoe_status; no C++ exception crosses the ABI.
+ * Host-side argument checks are synchronous.  Device work is enqueued on the
+ * handle's stream and is asynchronous unless stated otherwise.  Device-side
+ * faults (non-finite values, pair-capacity overflow) are latched on the
+ * device and reported by the next synchronising call (smoe_sync, smoe_step
+ * with stats, smoe_render to a host buffer).
+ *
+ * Memory: the caller owns params, targets, outputs and gradient buffers.
+ * Parameters must be DEVICE pointers (CUDA device memory of the handle's
+ * device).  `target` and `out` may be device or host pointers (host buffers
+ * are copied through a library staging buffer on the handle's stream; pinned
+ * host memory makes those copies asynchronous).  The library owns its
+ * workspace (kernel records, block lists, accumulators) and the Adam state and
+ * never frees caller memory.  A handle is bound to one device and one stream
+ * and is not thread-safe.
+ */
+#ifndef SMOE_H
+#define SMOE_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SMOE_ABI_VERSION 1
+
+typedef struct smoe_ctx *smoe_handle;
+
+typedef enum {
+    SMOE_OK = 0,
+    SMOE_ERR_INVALID_ARG = 1,   /* bad shape, NULL pointer, unsupported C/order   */
+    SMOE_ERR_CUDA = 2,          /* a CUDA runtime call failed (see smoe_last_error) */
+    SMOE_ERR_OUT_OF_MEMORY = 3, /* workspace allocation failed                      */
+    SMOE_ERR_NONFINITE = 4,     /* NaN/Inf in parameters, loss or gradients */
+    SMOE_ERR_CAPACITY = 5,      /* (block, kernel) pair list overflowed; buffers were
+                                   grown, the affected asynchronous calls were
+                                   skipped and must be repeated                    */
+    SMOE_ERR_BAD_HANDLE = 6
+} smoe_status;
+
+/* Kernel parameters, caller-owned DEVICE float32 arrays (struct of arrays):
+ *   mu[K][2]       centre (x, y) in source pixels             (Eq. 3, mu_j)
+ *   chol[K][3]     (l11, l21, l22), Sigma = L L^T, l11,l22>0
+ *   log_pi[K]      log gate weight, pi = exp(log_pi)          (Eq. 4, pi_j)
+ *   expert[K][C][E] E = 1: (m_c); E = 3: (m_c, Wx_c, Wy_c)    (Eq. 2, m_j(x)) */
+typedef struct {
+    float *mu;
+    float *chol;
+    float *log_pi;
+    float *expert;
+} smoe_params;
+
+/* Per-group Adam learning rates for one step, already scheduled by
+ * the caller (smoe_paper_lr gives the paper's schedule).  A rate of 0 freezes
+ * the group (its Adam moments still advance). */
+typedef struct {
+    float mu;      /* centres                    (0.01 -> 1e-5)      */
+    float chol;    /* Cholesky factors           (1e-3)              */
+    float log_pi;  /* gate log-weights           (Q11: 0, frozen)           */
+    float expert;  /* expert constants m_c       (1e-3)              */
+    float slope;   /* linear-expert slopes W     (Q13: 2e-4)                */
+} smoe_lr;
+
+/* Step statistics, measured by the step's own forward pass (before the
+ * parameter update).  loss = SSE/(H W C) (Q8); psnr_db = 10 log10(1/MSE) on
+ * [0,1]-clamped images; pairs = number of (block, kernel) list
+ * entries (sum_n |K_n|, "Avg. kernel" = pairs / n_tiles). */
+typedef struct {
+    double loss;
+    double psnr_db;
+    double sse;
+    double sse_clamped;
+    long long pairs;
+    long long uncovered_px;
+    long long n_tiles;
+} smoe_stats;
+
+typedef struct {
+    int K, H, W, C, expert_order;  /* C in {1,3}; expert_order in {0,1}           */
+    double R2;                     /* truncation radius^2; default 2 ln 100 (Q1) */
+    int device;                    /* CUDA device ordinal, -1 = current device   */
+    long long pair_capacity;       /* initial pair capacity, 0 = automatic        */
+} smoe_options;
+
+/* Fill `o` with the defaults (R2 = 2 ln 100, device = -1, automatic capacity). */
+smoe_status smoe_default_options(smoe_options *o);
+
+/* Create a handle for K kernels fitting an H x W x C image (B.json:
+ * smoe_create(K, H, W, C, expert_order)).  Allocates the workspace and the
+ * Adam state (zeroed, step t = 0) on the current device.  K, H, W >= 1. */
+smoe_status smoe_create(int K, int H, int W, int C, int expert_order, smoe_handle *out);
+smoe_status smoe_create_ex(const smoe_options *opt, smoe_handle *out);
+smoe_status smoe_destroy(smoe_handle h);
+
+/* Bind the handle to a CUDA stream (cudaStream_t passed as void*; NULL = the
+ * legacy default stream).  All later device work is ordered on it. */
+smoe_status smoe_set_stream(smoe_handle h, void *stream);
+
+/* Native super-resolution render (B.json smoe_render(params,
+ * out_H, out_W)): out[C][out_H][out_W] (planar float32) = y sampled at the
+ * source point ((j+1/2) W/out_W - 1/2, (i+1/2) H/out_H - 1/2) of every output
+ * pixel (Q16); out_H = H, out_W = W is the plain reconstruction.  Pure: does
+ * not touch Adam state.  `out` may be host (call returns after the copy and
+ * capacity check) or device (asynchronous). */
+smoe_status smoe_render(smoe_handle h, const smoe_params *p, int out_H, int out_W, float *out);
+
+/* One training iteration (B.json smoe_step(params, target, lr)): forward,
+ * MSE loss, analytic gradients of all kernel parameters, fused Adam update
+ * (beta = 0.9/0.999, eps = 1e-8, Q9) and clamp l11,l22 >= 1e-3, in
+ * place on `p`.  target[C][H][W] float32, host or device.  If `stats` is
+ * non-NULL the call synchronises and fills it (pre-update loss/PSNR);
+ * otherwise it is asynchronous. */
+smoe_status smoe_step(smoe_handle h, smoe_params *p, const float *target,
+                      const smoe_lr *lr, smoe_stats *stats);
+
+/* Multi-GPU band split (tile-row bands): restrict
+ * smoe_grad to block rows [tile_row0, tile_row1) of the ceil(H/16) rows.
+ * The loss normalisation stays 1/(H W C) of the full image, so per-band
+ * gradients add up to the full-image gradient.  (0, 0) = whole image. */
+smoe_status smoe_set_band(smoe_handle h, int tile_row0, int tile_row1);
+
+/* Gradient of the loss restricted to the current band: grad[K][Pk] float32
+ * with Pk = 6 + C E, per kernel (mu_x, mu_y, l11, l21, l22, log_pi, expert
+ * block in the expert layout); sums[3] float64 = (SSE, clamped SSE, uncovered
+ * pixels) of the band.  grad and sums may be host or device pointers. */
+smoe_status smoe_grad(smoe_handle h, const smoe_params *p, const float *target,
+                      float *grad, double *sums);
+
+/* Adam update with a caller-supplied gradient (e.g. all-reduced over ranks):
+ * same update and clamp as smoe_step.  grad[K][Pk] host or device. */
+smoe_status smoe_apply(smoe_handle h, smoe_params *p, const float *grad, const smoe_lr *lr);
+
+/* Zero the Adam moments and the step counter. */
+smoe_status smoe_reset_adam(smoe_handle h);
+
+/* Wait for the handle's stream and report latched device faults.  If `last`
+ * is non-NULL it receives the statistics of the most recent step/grad. */
+smoe_status smoe_sync(smoe_handle h, smoe_stats *last);
+
+/* Diagnostic view of the block binning on an out_H x out_W
+ * raster: tile_range[n_tiles+1] (int32, [start, end) of block n), ids[P]
+ * (int32 kernel ids, ascending within a block) and tilebox[K][4] int32
+ * (tx0, tx1, ty0, ty1; -1 when the box misses the raster).  Synchronous.
+ * Any output pointer may be NULL; ids must hold ids_cap entries.
+ * *n_pairs receives P. */
+smoe_status smoe_bin(smoe_handle h, const smoe_params *p, int out_H, int out_W,
+                     int *tile_range, int *ids, long long ids_cap, long long *n_pairs,
+                     int *tilebox);
+
+/* The paper's mu learning rate at 0-based step t of a T-step fit:
+ * 0.01 * (1e-3)^(t/T), and the fixed group rates. */
+smoe_lr smoe_paper_lr(int t, int T);
+
+/* Device-time profiling of the library's own launches (bench.py uses it to
+ * time the dominant kernel inside the timed region, on the handle's stream).
+ * smoe_profile_begin: record a CUDA event pair around each of the next
+ * max_launches launches; also count the (pixel, kernel) pairs the rasteriser
+ * tests and the pairs inside the truncation ellipse (the work units of the
+ * roofline).  smoe_profile_end: synchronise, return per-kernel
+ * totals in times[SMOE_KERNEL_COUNT] and the work counters, stop profiling. */
+enum {
+    SMOE_KERNEL_PREPROCESS = 0,
+    SMOE_KERNEL_SCAN = 1,
+    SMOE_KERNEL_SCATTER = 2,
+    SMOE_KERNEL_SORT = 3,
+    SMOE_KERNEL_RASTER_TRAIN = 4,
+    SMOE_KERNEL_RASTER_RENDER = 5,
+    SMOE_KERNEL_ADAM = 6,
+    SMOE_KERNEL_COUNT = 7
+};
+typedef struct {
+    double total_ms;
+    long long launches;
+} smoe_kernel_time;
+typedef struct {
+    long long tested_pairs;   /* valid pixel x listed kernel, forward sweep */
+    long long hit_pairs;      /* of those, d^2 <= R2                        */
+} smoe_work;
+smoe_status smoe_profile_begin(smoe_handle h, int max_launches);
+smoe_status smoe_profile_end(smoe_handle h, smoe_kernel_time *times, smoe_work *work);
+const char *smoe_kernel_name(int id);
+
+/* Number of device kernel launches issued by the library since creation. */
+long long smoe_launch_count(smoe_handle h);
+
+const char *smoe_status_string(smoe_status s);
+const char *smoe_last_error(smoe_handle h);
+int smoe_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SMOE_H */

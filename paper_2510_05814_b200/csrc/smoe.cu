@@ -1,0 +1,727 @@
+// smoe.cu -- host runtime and C ABI of the B200-native Rasterized SMoE path.
+//
+// The ABI is declared (and documented, with the paper passages it follows)
+// in include/smoe.h.  This file owns the workspace, the launch sequences of
+// §8(a) and the device-fault / capacity protocol.  No compute
+// happens on the host: every step of the path runs in smoe_kernels.cuh.
+#include "smoe.h"
+#include "smoe_kernels.cuh"
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+using namespace smoe;
+
+namespace {
+
+struct SmoeError : std::runtime_error {
+    smoe_status st;
+    SmoeError(smoe_status s, const std::string &m) : std::runtime_error(m), st(s) {}
+};
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess) {                                                          \
+            (void)cudaGetLastError();                                                     \
+            throw SmoeError(e_ == cudaErrorMemoryAllocation ? SMOE_ERR_OUT_OF_MEMORY       \
+                                                            : SMOE_ERR_CUDA,              \
+                            std::string(#call) + ": " + cudaGetErrorString(e_));         \
+        }                                                                                 \
+    } while (0)
+
+// Device-resident control block: one D2H copy brings back every counter.
+struct Ctl {
+    double dstats[4];   // SSE, clamped SSE, uncovered pixels, (unused)
+    GridCtr train;
+    GridCtr render;
+    HandleCtr hc;
+};
+
+struct Prof {
+    bool on = false;
+    int max = 0, n = 0;
+    std::vector<cudaEvent_t> ev;
+    std::vector<int> kid;
+    unsigned long long *d_work = nullptr;
+};
+
+struct Grid {
+    int oH = 0, oW = 0, nx = 0, ny = 0, n_tiles = 0;
+    int *cnt = nullptr, *start = nullptr, *cursor = nullptr;
+    int *ids = nullptr, *tmp = nullptr;
+    long long cap = 0;
+    bool calibrated = false;
+    GridCtr *gc = nullptr;   // points into Ctl
+};
+
+}  // namespace
+
+struct smoe_ctx {
+    int K, H, W, C, order, E, P, RS, V;
+    float R2;
+    int device;
+    cudaStream_t stream = nullptr;
+    float *rec = nullptr;
+    int4 *tbox = nullptr;
+    float *acc = nullptr, *m1 = nullptr, *m2 = nullptr;
+    Ctl *ctl = nullptr;      // device
+    Ctl *h_ctl = nullptr;    // pinned host mirror
+    float *stage_in = nullptr;  size_t stage_in_n = 0;
+    float *stage_out = nullptr; size_t stage_out_n = 0;
+    double *stage_sums = nullptr;
+    Grid train, render;
+    int band0 = 0, band1 = 0;   // tile rows; band1 == 0 -> whole image
+    long long launches = 0;
+    long long init_cap = 0;
+    Prof prof;
+    std::string err;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+void set_err(smoe_ctx *h, const std::string &m)
+{
+    if (h) h->err = m;
+    g_err = m;
+}
+
+template <class F>
+smoe_status guard(smoe_ctx *h, F &&f)
+{
+    try {
+        if (h) CK(cudaSetDevice(h->device));
+        return f();
+    } catch (SmoeError &e) {
+        set_err(h, e.what());
+        return e.st;
+    } catch (std::bad_alloc &) {
+        set_err(h, "host allocation failed");
+        return SMOE_ERR_OUT_OF_MEMORY;
+    } catch (std::exception &e) {
+        set_err(h, e.what());
+        return SMOE_ERR_CUDA;
+    }
+}
+
+void check_launch(smoe_ctx *h, const char *what)
+{
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw SmoeError(SMOE_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    h->launches++;
+}
+
+// Launch with optional profiling events around it (same stream).
+template <class F>
+void launch(smoe_ctx *h, int kid, const char *what, F &&f)
+{
+    Prof &P = h->prof;
+    bool rec = P.on && P.n < P.max;
+    if (rec) CK(cudaEventRecord(P.ev[2 * P.n], h->stream));
+    f();
+    check_launch(h, what);
+    if (rec) {
+        CK(cudaEventRecord(P.ev[2 * P.n + 1], h->stream));
+        P.kid[P.n] = kid;
+        P.n++;
+    }
+}
+
+bool is_device_ptr(const void *p)
+{
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+template <class T>
+void dfree(T *&p)
+{
+    if (p) cudaFree((void *)p);
+    p = nullptr;
+}
+
+void free_grid(Grid &g)
+{
+    dfree(g.cnt); dfree(g.start); dfree(g.cursor); dfree(g.ids); dfree(g.tmp);
+    g = Grid();
+}
+
+float *stage(float *&buf, size_t &have, size_t n)
+{
+    if (have < n) {
+        dfree(buf);
+        CK(cudaMalloc(&buf, n * sizeof(float)));
+        have = n;
+    }
+    return buf;
+}
+
+void ensure_grid(smoe_ctx *h, Grid &g, GridCtr *gc, int oH, int oW)
+{
+    if (g.oH == oH && g.oW == oW && g.cnt) return;
+    long long cap = g.cap;
+    bool cal = g.calibrated && g.oH == oH && g.oW == oW;
+    dfree(g.cnt); dfree(g.start); dfree(g.cursor);
+    g.oH = oH; g.oW = oW;
+    g.nx = (oW + TILE - 1) / TILE;
+    g.ny = (oH + TILE - 1) / TILE;
+    g.n_tiles = g.nx * g.ny;
+    g.gc = gc;
+    CK(cudaMalloc(&g.cnt, sizeof(int) * g.n_tiles));
+    CK(cudaMalloc(&g.start, sizeof(int) * (g.n_tiles + 1)));
+    CK(cudaMalloc(&g.cursor, sizeof(int) * g.n_tiles));
+    CK(cudaMemsetAsync(g.cnt, 0, sizeof(int) * g.n_tiles, h->stream));
+    CK(cudaMemsetAsync(gc, 0, sizeof(GridCtr), h->stream));
+    g.cap = cap;
+    g.calibrated = cal;
+}
+
+void grow(smoe_ctx *h, Grid &g, long long need)
+{
+    long long cap = need + need / 4 + 4096;
+    dfree(g.ids); dfree(g.tmp);
+    CK(cudaMalloc(&g.ids, sizeof(int) * cap));
+    CK(cudaMalloc(&g.tmp, sizeof(int) * cap));
+    g.cap = cap;
+    g.calibrated = true;
+    CK(cudaMemsetAsync(&g.gc->need, 0, 2 * sizeof(long long), h->stream));  // need, skipped
+}
+
+void read_ctl(smoe_ctx *h)
+{
+    CK(cudaMemcpyAsync(h->h_ctl, h->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+}
+
+#define DISPATCH_CE(h, BODY)                                                  \
+    do {                                                                      \
+        if (h->C == 1 && h->E == 1) { constexpr int C_ = 1, E_ = 1; BODY; }   \
+        else if (h->C == 1 && h->E == 3) { constexpr int C_ = 1, E_ = 3; BODY; } \
+        else if (h->C == 3 && h->E == 1) { constexpr int C_ = 3, E_ = 1; BODY; } \
+        else { constexpr int C_ = 3, E_ = 3; BODY; }                          \
+    } while (0)
+
+ParamsDev pdev(const smoe_params *p) { return ParamsDev{p->mu, p->chol, p->log_pi, p->expert}; }
+
+void check_params(const smoe_params *p)
+{
+    if (!p || !p->mu || !p->chol || !p->log_pi || !p->expert)
+        throw SmoeError(SMOE_ERR_INVALID_ARG, "params: NULL pointer");
+    if (!is_device_ptr(p->mu) || !is_device_ptr(p->chol) || !is_device_ptr(p->log_pi) || !is_device_ptr(p->expert))
+        throw SmoeError(SMOE_ERR_INVALID_ARG, "params must be device pointers");
+    if (((uintptr_t)p->mu & 7) != 0) throw SmoeError(SMOE_ERR_INVALID_ARG, "params.mu must be 8-byte aligned");
+}
+
+// a1-a4: preprocess, scan, scatter, in-bucket sort on grid g for block rows
+// [ty_lo, ty_hi).  The first binning of a grid calibrates the capacity with
+// one synchronous read of P; later binnings never synchronise.
+void bin(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_hi, bool zero_stats)
+{
+    int K = h->K;
+    int nb = (K + 255) / 256;
+    float sx = (float)g.oW / (float)h->W, sy = (float)g.oH / (float)h->H;
+    launch(h, SMOE_KERNEL_PREPROCESS, "k_preprocess", [&] {
+        DISPATCH_CE(h, (k_preprocess<C_, E_><<<nb, 256, 0, h->stream>>>(
+                           K, pdev(p), h->R2, sx, sy, g.oW, g.oH, g.nx, ty_lo, ty_hi, h->rec, h->tbox,
+                           g.cnt, &h->ctl->hc)));
+    });
+    launch(h, SMOE_KERNEL_SCAN, "k_scan", [&] {
+        k_scan<<<1, 1024, 0, h->stream>>>(g.cnt, g.n_tiles, g.start, g.cursor, g.cap, g.gc,
+                                          zero_stats ? h->ctl->dstats : nullptr);
+    });
+    if (!g.calibrated) {
+        long long P;
+        CK(cudaMemcpyAsync(&P, &g.gc->pairs, sizeof(P), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        grow(h, g, P > h->init_cap ? P : h->init_cap);
+    }
+    launch(h, SMOE_KERNEL_SCATTER, "k_scatter", [&] {
+        k_scatter<<<nb, 256, 0, h->stream>>>(K, h->tbox, g.nx, ty_lo, ty_hi, g.cursor, g.ids, g.cap, g.gc);
+    });
+    int nt = (ty_hi - ty_lo) * g.nx;
+    if (nt > 0) {
+        launch(h, SMOE_KERNEL_SORT, "k_sort_segs", [&] {
+            k_sort_segs<<<nt, 256, 0, h->stream>>>(g.start, g.ids, g.tmp, ty_lo * g.nx, g.cap, g.gc);
+        });
+    }
+}
+
+void band_rows(smoe_ctx *h, int &ty_lo, int &ty_hi)
+{
+    int ny = (h->H + TILE - 1) / TILE;
+    if (h->band1 > h->band0) { ty_lo = h->band0; ty_hi = h->band1; }
+    else { ty_lo = 0; ty_hi = ny; }
+}
+
+const float *stage_target(smoe_ctx *h, const float *target)
+{
+    if (is_device_ptr(target)) return target;
+    size_t n = (size_t)h->C * h->H * h->W;
+    float *d = stage(h->stage_in, h->stage_in_n, n);
+    CK(cudaMemcpyAsync(d, target, n * sizeof(float), cudaMemcpyHostToDevice, h->stream));
+    return d;
+}
+
+// a1-a7 on the training grid (current band): raw sums into h->acc, loss
+// partials into ctl->dstats.
+void forward_backward(smoe_ctx *h, const smoe_params *p, const float *target)
+{
+    Grid &g = h->train;
+    ensure_grid(h, g, &h->ctl->train, h->H, h->W);
+    int ty_lo, ty_hi;
+    band_rows(h, ty_lo, ty_hi);
+    bin(h, g, p, ty_lo, ty_hi, true);
+    int nt = (ty_hi - ty_lo) * g.nx;
+    if (nt <= 0) return;
+    RasterArgs A{};
+    A.rec = h->rec; A.ids = g.ids; A.start = g.start; A.gc = g.gc; A.cap = g.cap;
+    A.nx = g.nx; A.tile0 = ty_lo * g.nx; A.oW = h->W; A.oH = h->H;
+    A.sx = 1.0f; A.sy = 1.0f; A.R2 = h->R2;
+    A.target = target;
+    A.e_scale = (float)(2.0 / ((double)h->H * h->W * h->C));
+    A.acc = h->acc; A.dstats = h->ctl->dstats; A.out = nullptr;
+    A.work = h->prof.d_work;
+    launch(h, SMOE_KERNEL_RASTER_TRAIN, "k_raster<train>", [&] {
+        if (h->prof.on) DISPATCH_CE(h, (k_raster<C_, E_, true, true><<<nt, 128, 0, h->stream>>>(A)));
+        else DISPATCH_CE(h, (k_raster<C_, E_, true, false><<<nt, 128, 0, h->stream>>>(A)));
+    });
+}
+
+void launch_adam(smoe_ctx *h, int mode, const smoe_params *p, const float *grad_in, float *grad_out,
+                 const smoe_lr *lr)
+{
+    int K = h->K;
+    int nb = (K + 255) / 256;
+    ParamsMut pm{p->mu, p->chol, p->log_pi, p->expert};
+    LrDev l{0, 0, 0, 0, 0};
+    if (lr) l = LrDev{lr->mu, lr->chol, lr->log_pi, lr->expert, lr->slope};
+    const GridCtr *gc = &h->ctl->train;
+    long long cap = h->train.cap;
+    launch(h, SMOE_KERNEL_ADAM, "k_adam", [&] {
+        if (mode == 0)
+            DISPATCH_CE(h, (k_adam<C_, E_, 0><<<nb, 256, 0, h->stream>>>(K, pm, h->acc, nullptr, nullptr, h->m1,
+                                                                           h->m2, l, &h->ctl->hc, gc, cap)));
+        else if (mode == 1)
+            DISPATCH_CE(h, (k_adam<C_, E_, 1><<<nb, 256, 0, h->stream>>>(K, pm, h->acc, nullptr, grad_out, h->m1,
+                                                                           h->m2, l, &h->ctl->hc, gc, cap)));
+        else
+            DISPATCH_CE(h, (k_adam<C_, E_, 2><<<nb, 256, 0, h->stream>>>(K, pm, h->acc, grad_in, nullptr, h->m1,
+                                                                           h->m2, l, &h->ctl->hc, gc, cap)));
+    });
+}
+
+// Inspect the latched device faults after a synchronisation point.
+smoe_status faults(smoe_ctx *h, Grid *g_overflow_report = nullptr)
+{
+    Ctl &c = *h->h_ctl;
+    if (c.hc.nonfinite) {
+        CK(cudaMemsetAsync(&h->ctl->hc.nonfinite, 0, sizeof(long long), h->stream));
+        set_err(h, "non-finite parameter or gradient detected on the device");
+        return SMOE_ERR_NONFINITE;
+    }
+    smoe_status st = SMOE_OK;
+    Grid *gs[2] = {&h->train, &h->render};
+    GridCtr *cs[2] = {&c.train, &c.render};
+    for (int i = 0; i < 2; i++) {
+        if (cs[i]->need > gs[i]->cap && gs[i]->ids) {
+            long long skipped = cs[i]->skipped;
+            grow(h, *gs[i], cs[i]->need);
+            set_err(h, "pair capacity exceeded; grown to " + std::to_string(gs[i]->cap) + ", " +
+                           std::to_string(skipped) + " call(s) skipped");
+            st = SMOE_ERR_CAPACITY;
+        }
+    }
+    (void)g_overflow_report;
+    return st;
+}
+
+void fill_stats(smoe_ctx *h, smoe_stats *s)
+{
+    Ctl &c = *h->h_ctl;
+    double n = (double)h->H * h->W * h->C;
+    s->sse = c.dstats[0];
+    s->sse_clamped = c.dstats[1];
+    s->uncovered_px = (long long)c.dstats[2];
+    s->loss = c.dstats[0] / n;
+    double mse_c = c.dstats[1] / n;
+    s->psnr_db = mse_c > 0 ? 10.0 * std::log10(1.0 / mse_c) : INFINITY;
+    s->pairs = c.train.pairs;
+    s->n_tiles = h->train.n_tiles;
+}
+
+}  // namespace
+
+// ============================================================== C ABI =====
+extern "C" {
+
+int smoe_abi_version(void) { return SMOE_ABI_VERSION; }
+
+const char *smoe_status_string(smoe_status s)
+{
+    switch (s) {
+    case SMOE_OK: return "ok";
+    case SMOE_ERR_INVALID_ARG: return "invalid argument";
+    case SMOE_ERR_CUDA: return "CUDA error";
+    case SMOE_ERR_OUT_OF_MEMORY: return "out of memory";
+    case SMOE_ERR_NONFINITE: return "non-finite value";
+    case SMOE_ERR_CAPACITY: return "pair capacity exceeded";
+    case SMOE_ERR_BAD_HANDLE: return "bad handle";
+    }
+    return "unknown status";
+}
+
+const char *smoe_last_error(smoe_handle h) { return h ? h->err.c_str() : g_err.c_str(); }
+
+smoe_status smoe_default_options(smoe_options *o)
+{
+    if (!o) return SMOE_ERR_INVALID_ARG;
+    std::memset(o, 0, sizeof(*o));
+    o->C = 3;
+    o->R2 = 2.0 * std::log(100.0);   // chi2_2(0.99) (Q1)
+    o->device = -1;
+    return SMOE_OK;
+}
+
+smoe_lr smoe_paper_lr(int t, int T)
+{
+    smoe_lr l;
+    double frac = T > 0 ? (double)t / T : 0.0;
+    l.mu = (float)(0.01 * std::pow(1e-3, frac));   // 0.01 -> 1e-5
+    l.chol = 1e-3f;
+    l.log_pi = 0.0f;                               // Q11 frozen
+    l.expert = 1e-3f;
+    l.slope = 2e-4f;                               // Q13
+    return l;
+}
+
+smoe_status smoe_create_ex(const smoe_options *o, smoe_handle *out)
+{
+    if (!o || !out) { g_err = "NULL argument"; return SMOE_ERR_INVALID_ARG; }
+    *out = nullptr;
+    if (o->K < 1 || o->H < 1 || o->W < 1 || !(o->C == 1 || o->C == 3) ||
+        !(o->expert_order == 0 || o->expert_order == 1) || !(o->R2 > 0)) {
+        g_err = "smoe_create: need K,H,W >= 1, C in {1,3}, expert_order in {0,1}, R2 > 0";
+        return SMOE_ERR_INVALID_ARG;
+    }
+    if ((long long)o->H * o->W >= (1ll << 31) || o->K >= (1 << 30)) {
+        g_err = "smoe_create: image or kernel count too large";
+        return SMOE_ERR_INVALID_ARG;
+    }
+    smoe_ctx *h = new (std::nothrow) smoe_ctx();
+    if (!h) return SMOE_ERR_OUT_OF_MEMORY;
+    h->K = o->K; h->H = o->H; h->W = o->W; h->C = o->C; h->order = o->expert_order;
+    h->E = 1 + 2 * h->order;
+    h->P = 6 + h->C * h->E;
+    h->RS = (h->P + 3) & ~3;
+    h->V = h->P <= 8 ? 8 : 16;
+    h->R2 = (float)o->R2;
+    h->init_cap = o->pair_capacity;
+    int dev = o->device;
+    if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) {
+        (void)cudaGetLastError();
+        g_err = "no CUDA device";
+        delete h;
+        return SMOE_ERR_CUDA;
+    }
+    h->device = dev;
+    smoe_status st = guard(h, [&]() {
+        size_t K = h->K;
+        CK(cudaMalloc(&h->rec, K * h->RS * sizeof(float)));
+        CK(cudaMalloc(&h->tbox, K * sizeof(int4)));
+        CK(cudaMalloc(&h->acc, K * h->V * sizeof(float)));
+        CK(cudaMalloc(&h->m1, K * h->P * sizeof(float)));
+        CK(cudaMalloc(&h->m2, K * h->P * sizeof(float)));
+        CK(cudaMalloc(&h->ctl, sizeof(Ctl)));
+        CK(cudaMallocHost(&h->h_ctl, sizeof(Ctl)));
+        CK(cudaMalloc(&h->stage_sums, 4 * sizeof(double)));
+        CK(cudaMemset(h->acc, 0, K * h->V * sizeof(float)));
+        CK(cudaMemset(h->m1, 0, K * h->P * sizeof(float)));
+        CK(cudaMemset(h->m2, 0, K * h->P * sizeof(float)));
+        CK(cudaMemset(h->ctl, 0, sizeof(Ctl)));
+        std::memset(h->h_ctl, 0, sizeof(Ctl));
+        CK(cudaDeviceSynchronize());
+        return SMOE_OK;
+    });
+    if (st != SMOE_OK) {
+        g_err = h->err;
+        smoe_destroy(h);
+        return st;
+    }
+    *out = h;
+    return SMOE_OK;
+}
+
+smoe_status smoe_create(int K, int H, int W, int C, int expert_order, smoe_handle *out)
+{
+    smoe_options o;
+    smoe_default_options(&o);
+    o.K = K; o.H = H; o.W = W; o.C = C; o.expert_order = expert_order;
+    return smoe_create_ex(&o, out);
+}
+
+smoe_status smoe_destroy(smoe_handle h)
+{
+    if (!h) return SMOE_ERR_BAD_HANDLE;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    else cudaDeviceSynchronize();
+    free_grid(h->train);
+    free_grid(h->render);
+    dfree(h->rec); dfree(h->tbox); dfree(h->acc); dfree(h->m1); dfree(h->m2);
+    dfree(h->ctl); dfree(h->stage_in); dfree(h->stage_out); dfree(h->stage_sums);
+    if (h->h_ctl) cudaFreeHost(h->h_ctl);
+    for (cudaEvent_t e : h->prof.ev) cudaEventDestroy(e);
+    dfree(h->prof.d_work);
+    (void)cudaGetLastError();
+    delete h;
+    return SMOE_OK;
+}
+
+smoe_status smoe_set_stream(smoe_handle h, void *stream)
+{
+    if (!h) return SMOE_ERR_BAD_HANDLE;
+    h->stream = (cudaStream_t)stream;
+    return SMOE_OK;
+}
+
+smoe_status smoe_set_band(smoe_handle h, int r0, int r1)
+{
+    if (!h) return SMOE_ERR_BAD_HANDLE;
+    int ny = (h->H + TILE - 1) / TILE;
+    if (r0 == 0 && r1 == 0) { h->band0 = h->band1 = 0; return SMOE_OK; }
+    if (r0 < 0 || r1 > ny || r0 >= r1) {
+        set_err(h, "smoe_set_band: need 0 <= row0 < row1 <= ceil(H/16)");
+        return SMOE_ERR_INVALID_ARG;
+    }
+    h->band0 = r0; h->band1 = r1;
+    return SMOE_OK;
+}
+
+smoe_status smoe_reset_adam(smoe_handle h)
+{
+    if (!h) return SMOE_ERR_BAD_HANDLE;
+    return guard(h, [&]() {
+        CK(cudaMemsetAsync(h->m1, 0, (size_t)h->K * h->P * sizeof(float), h->stream));
+        CK(cudaMemsetAsync(h->m2, 0, (size_t)h->K * h->P * sizeof(float), h->stream));
+        CK(cudaMemsetAsync(&h->ctl->hc, 0, sizeof(HandleCtr), h->stream));
+        return SMOE_OK;
+    });
+}
+
+smoe_status smoe_sync(smoe_handle h, smoe_stats *last)
+{
+    if (!h) return SMOE_ERR_BAD_HANDLE;
+    return guard(h, [&]() {
+        read_ctl(h);
+        if (last) fill_stats(h, last);
+        return faults(h);
+    });
+}
+
+smoe_status smoe_step(smoe_handle h, smoe_params *p, const float *target, const smoe_lr *lr,
+                      smoe_stats *stats)
+{
+    if (!h) return SMOE_ERR_BAD_HANDLE;
+    return guard(h, [&]() -> smoe_status {
+        check_params(p);
+        if (!target || !lr) throw SmoeError(SMOE_ERR_INVALID_ARG, "smoe_step: NULL target or lr");
+        for (int attempt = 0;; attempt++) {
+            const float *t = stage_target(h, target);
+            forward_backward(h, p, t);
+            launch_adam(h, 0, p, nullptr, nullptr, lr);
+            if (!stats) return SMOE_OK;
+            read_ctl(h);
+            smoe_status st = faults(h);
+            if (st == SMOE_ERR_CAPACITY && attempt < 3) continue;   // grown: redo the skipped step
+            fill_stats(h, stats);
+            return st;
+        }
+    });
+}
+
+smoe_status smoe_grad(smoe_handle h, const smoe_params *p, const float *target, float *grad, double *sums)
+{
+    if (!h) return SMOE_ERR_BAD_HANDLE;
+    return guard(h, [&]() -> smoe_status {
+        check_params(p);
+        if (!target || !grad) throw SmoeError(SMOE_ERR_INVALID_ARG, "smoe_grad: NULL target or grad");
+        bool gdev = is_device_ptr(grad);
+        bool sdev = sums ? is_device_ptr(sums) : true;
+        for (int attempt = 0;; attempt++) {
+            const float *t = stage_target(h, target);
+            forward_backward(h, p, t);
+            size_t n = (size_t)h->K * h->P;
+            float *gout = gdev ? grad : stage(h->stage_out, h->stage_out_n, n);
+            launch_adam(h, 1, p, nullptr, gout, nullptr);
+            if (gdev && sdev) {
+                if (sums)
+                    CK(cudaMemcpyAsync(sums, h->ctl->dstats, 3 * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+                return SMOE_OK;
+            }
+            read_ctl(h);
+            smoe_status st = faults(h);
+            if (st == SMOE_ERR_CAPACITY && attempt < 3) continue;
+            if (!gdev) {
+                CK(cudaMemcpyAsync(grad, gout, n * sizeof(float), cudaMemcpyDeviceToHost, h->stream));
+                CK(cudaStreamSynchronize(h->stream));
+            }
+            if (sums) {
+                if (sdev) CK(cudaMemcpy(sums, h->ctl->dstats, 3 * sizeof(double), cudaMemcpyDeviceToDevice));
+                else std::memcpy(sums, h->h_ctl->dstats, 3 * sizeof(double));
+            }
+            return st;
+        }
+    });
+}
+
+smoe_status smoe_apply(smoe_handle h, smoe_params *p, const float *grad, const smoe_lr *lr)
+{
+    if (!h) return SMOE_ERR_BAD_HANDLE;
+    return guard(h, [&]() -> smoe_status {
+        check_params(p);
+        if (!grad || !lr) throw SmoeError(SMOE_ERR_INVALID_ARG, "smoe_apply: NULL grad or lr");
+        const float *g = grad;
+        if (!is_device_ptr(grad)) {
+            size_t n = (size_t)h->K * h->P;
+            float *d = stage(h->stage_in, h->stage_in_n, n);
+            CK(cudaMemcpyAsync(d, grad, n * sizeof(float), cudaMemcpyHostToDevice, h->stream));
+            g = d;
+        }
+        launch_adam(h, 2, p, g, nullptr, lr);
+        return SMOE_OK;
+    });
+}
+
+smoe_status smoe_render(smoe_handle h, const smoe_params *p, int out_H, int out_W, float *out)
+{
+    if (!h) return SMOE_ERR_BAD_HANDLE;
+    return guard(h, [&]() -> smoe_status {
+        check_params(p);
+        if (!out || out_H < 1 || out_W < 1 || (long long)out_H * out_W >= (1ll << 31))
+            throw SmoeError(SMOE_ERR_INVALID_ARG, "smoe_render: bad output");
+        bool odev = is_device_ptr(out);
+        for (int attempt = 0;; attempt++) {
+            Grid &g = h->render;
+            ensure_grid(h, g, &h->ctl->render, out_H, out_W);
+            bin(h, g, p, 0, g.ny, false);
+            size_t n = (size_t)h->C * out_H * out_W;
+            float *o = odev ? out : stage(h->stage_out, h->stage_out_n, n);
+            RasterArgs A{};
+            A.rec = h->rec; A.ids = g.ids; A.start = g.start; A.gc = g.gc; A.cap = g.cap;
+            A.nx = g.nx; A.tile0 = 0; A.oW = out_W; A.oH = out_H;
+            A.sx = (float)h->W / (float)out_W; A.sy = (float)h->H / (float)out_H;
+            A.R2 = h->R2; A.out = o;
+            A.work = h->prof.d_work;
+            launch(h, SMOE_KERNEL_RASTER_RENDER, "k_raster<render>", [&] {
+                if (h->prof.on) DISPATCH_CE(h, (k_raster<C_, E_, false, true><<<g.n_tiles, 128, 0, h->stream>>>(A)));
+                else DISPATCH_CE(h, (k_raster<C_, E_, false, false><<<g.n_tiles, 128, 0, h->stream>>>(A)));
+            });
+            if (odev) return SMOE_OK;
+            read_ctl(h);
+            smoe_status st = faults(h);
+            if (st == SMOE_ERR_CAPACITY && attempt < 3) continue;
+            CK(cudaMemcpyAsync(out, o, n * sizeof(float), cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+            return st;
+        }
+    });
+}
+
+smoe_status smoe_bin(smoe_handle h, const smoe_params *p, int out_H, int out_W, int *tile_range, int *ids,
+                     long long ids_cap, long long *n_pairs, int *tilebox)
+{
+    if (!h) return SMOE_ERR_BAD_HANDLE;
+    return guard(h, [&]() -> smoe_status {
+        check_params(p);
+        if (out_H < 1 || out_W < 1) throw SmoeError(SMOE_ERR_INVALID_ARG, "smoe_bin: bad raster");
+        for (int attempt = 0;; attempt++) {
+            Grid &g = h->render;
+            ensure_grid(h, g, &h->ctl->render, out_H, out_W);
+            bin(h, g, p, 0, g.ny, false);
+            read_ctl(h);
+            smoe_status st = faults(h);
+            if (st == SMOE_ERR_CAPACITY && attempt < 3) continue;
+            if (st != SMOE_OK) return st;
+            long long P = h->h_ctl->render.pairs;
+            if (n_pairs) *n_pairs = P;
+            if (tile_range)
+                CK(cudaMemcpy(tile_range, g.start, sizeof(int) * (g.n_tiles + 1), cudaMemcpyDefault));
+            if (ids) {
+                if (ids_cap < P) throw SmoeError(SMOE_ERR_INVALID_ARG, "smoe_bin: ids_cap < P");
+                CK(cudaMemcpy(ids, g.ids, sizeof(int) * P, cudaMemcpyDefault));
+            }
+            if (tilebox) CK(cudaMemcpy(tilebox, h->tbox, sizeof(int4) * h->K, cudaMemcpyDefault));
+            return SMOE_OK;
+        }
+    });
+}
+
+long long smoe_launch_count(smoe_handle h) { return h ? h->launches : -1; }
+
+const char *smoe_kernel_name(int id)
+{
+    static const char *names[SMOE_KERNEL_COUNT] = {"k_preprocess", "k_scan", "k_scatter", "k_sort_segs",
+                                                   "k_raster<train>", "k_raster<render>", "k_adam"};
+    return (id >= 0 && id < SMOE_KERNEL_COUNT) ? names[id] : "?";
+}
+
+smoe_status smoe_profile_begin(smoe_handle h, int max_launches)
+{
+    if (!h) return SMOE_ERR_BAD_HANDLE;
+    if (max_launches < 1) { set_err(h, "max_launches < 1"); return SMOE_ERR_INVALID_ARG; }
+    return guard(h, [&]() {
+        Prof &P = h->prof;
+        while ((int)P.ev.size() < 2 * max_launches) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            P.ev.push_back(e);
+        }
+        P.kid.assign(max_launches, -1);
+        P.max = max_launches;
+        P.n = 0;
+        if (!P.d_work) CK(cudaMalloc(&P.d_work, 2 * sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(P.d_work, 0, 2 * sizeof(unsigned long long), h->stream));
+        P.on = true;
+        return SMOE_OK;
+    });
+}
+
+smoe_status smoe_profile_end(smoe_handle h, smoe_kernel_time *times, smoe_work *work)
+{
+    if (!h) return SMOE_ERR_BAD_HANDLE;
+    return guard(h, [&]() {
+        Prof &P = h->prof;
+        CK(cudaStreamSynchronize(h->stream));
+        if (times) {
+            for (int i = 0; i < SMOE_KERNEL_COUNT; i++) times[i] = smoe_kernel_time{0.0, 0};
+            for (int i = 0; i < P.n; i++) {
+                float ms = 0.f;
+                CK(cudaEventElapsedTime(&ms, P.ev[2 * i], P.ev[2 * i + 1]));
+                times[P.kid[i]].total_ms += ms;
+                times[P.kid[i]].launches += 1;
+            }
+        }
+        if (work) {
+            unsigned long long w[2] = {0, 0};
+            if (P.d_work) CK(cudaMemcpy(w, P.d_work, sizeof(w), cudaMemcpyDeviceToHost));
+            work->tested_pairs = (long long)w[0];
+            work->hit_pairs = (long long)w[1];
+        }
+        P.on = false;
+        P.n = 0;
+        return SMOE_OK;
+    });
+}
+
+}  // extern "C"

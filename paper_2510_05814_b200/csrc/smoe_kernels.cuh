@@ -1,0 +1,643 @@
+// smoe_kernels.cuh -- sm_100a device code of the Rasterized SMoE hot path.
+//
+// Citations: P:n = PAPER.md line n (arxiv 2510.05814), S:n = SPEC.md line n,
+// Q-numbers = readings in DESIGN.md.  Pipeline of one step:
+//
+//   k_preprocess  per kernel: whitening record, square 99% box,
+//                 per-block overlap counts (atomics)             [§8(a) a1]
+//   k_scan        exclusive scan of block counts -> block ranges  [a2/a4]
+//   k_scatter     kernel ids into their blocks' buckets           [a3]
+//   k_sort_segs   in-bucket sort by kernel id (second radix digit)[a4]
+//   k_raster      per 16x16 block: forward, loss, backward         [a5-a7, a9]
+//   k_adam        chain rule -> Adam -> clamp, accumulator reset   [a8]
+//
+// The binning is an MSD radix sort of the key (tile_id | kernel_id): the
+// first digit (the whole tile id) is a counting sort driven by per-block
+// atomics, the second (kernel id) an in-shared-memory sort per bucket.  The
+// result is the canonical list K_n (Eq. 5): blocks ascending, kernel ids
+// ascending inside a block (Q18).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace smoe {
+
+constexpr int TILE = 16;                 // 16x16 blocks
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int SORT_CAP = 2048;           // bucket size sorted in one smem pass
+
+// Per-grid device counters (one block grid = one raster: the training image
+// or one render resolution).
+struct GridCtr {
+    long long pairs;      // P of the most recent binning on this grid
+    long long need;       // latched: largest P that exceeded the capacity
+    long long skipped;    // latched: sequences skipped because of overflow
+};
+
+// Per-handle device counters.
+struct HandleCtr {
+    long long t;          // Adam step counter (1-based after the first step)
+    long long nonfinite;  // latched non-finite flag (S:355 DivergedLoss)
+    unsigned int done;    // last-block ticket of k_adam
+    unsigned int pad;
+};
+
+struct ParamsDev {
+    const float *mu, *chol, *log_pi, *expert;
+};
+struct ParamsMut {
+    float *mu, *chol, *log_pi, *expert;
+};
+struct LrDev {
+    float mu, chol, log_pi, expert, slope;
+};
+
+// Record stride (floats) of the per-kernel render record:
+// [mu_x, mu_y, a, b, c, log_pi*log2e, expert(C*E)] padded to float4.
+template <int C, int E>
+struct Rec {
+    static constexpr int P = 6 + C * E;          // parameters per kernel
+    static constexpr int RS = (P + 3) & ~3;      // record stride, floats
+    static constexpr int V = P <= 8 ? 8 : 16;    // accumulator stride (pow2)
+};
+
+__device__ __forceinline__ float ex2_approx(float x)
+{
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ bool finitef(float x) { return isfinite(x); }
+
+// ---------------------------------------------------------------- a1 ------
+// Geometry shader: Sigma = L L^T, lambda_max in closed form,
+// square box of half side r = sqrt(R2 lambda_max), pixel-centre rule (Q5)
+// on the out_H x out_W raster, then the per-block overlap counts for the
+// block rows [ty_lo, ty_hi) (the whole grid, or one multi-GPU band).
+// Whitening: u = a dx, v = b dx + c dy with a = 1/l11, b = -l21/(l11 l22),
+// c = 1/l22, so d^2 = u^2 + v^2 = delta^T Sigma^-1 delta.
+template <int C, int E>
+__global__ void __launch_bounds__(256)
+k_preprocess(int K, ParamsDev p, float R2, float sx /* oW/W */, float sy /* oH/H */, int oW, int oH,
+             int nx, int ty_lo, int ty_hi, float *__restrict__ rec,
+             int4 *__restrict__ tbox, int *__restrict__ cnt, HandleCtr *hc)
+{
+    using R = Rec<C, E>;
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    float2 mu = reinterpret_cast<const float2 *>(p.mu)[k];
+    float l11 = p.chol[3 * k], l21 = p.chol[3 * k + 1], l22 = p.chol[3 * k + 2];
+    float lp = p.log_pi[k];
+    float a = 1.0f / l11, c = 1.0f / l22;
+    float b = -l21 / (l11 * l22);
+    float r[R::RS];
+    r[0] = mu.x; r[1] = mu.y; r[2] = a; r[3] = b; r[4] = c; r[5] = lp * LOG2E;
+    bool ok = finitef(mu.x) && finitef(mu.y) && finitef(a) && finitef(b) && finitef(c) && finitef(lp);
+#pragma unroll
+    for (int i = 0; i < C * E; i++) {
+        r[6 + i] = p.expert[(size_t)k * C * E + i];
+        ok = ok && finitef(r[6 + i]);
+    }
+#pragma unroll
+    for (int i = R::P; i < R::RS; i++) r[i] = 0.0f;
+    float4 *dst = reinterpret_cast<float4 *>(rec) + (size_t)k * (R::RS / 4);
+#pragma unroll
+    for (int q = 0; q < R::RS / 4; q++) dst[q] = make_float4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+    if (!ok) atomicExch((unsigned long long *)&hc->nonfinite, 1ull);
+
+    float s11 = l11 * l11, s12 = l11 * l21, s22 = l21 * l21 + l22 * l22;
+    float h = 0.5f * (s11 - s22);
+    float lmax = 0.5f * (s11 + s22) + sqrtf(h * h + s12 * s12);
+    float rr = sqrtf(R2 * lmax);
+    float xl = ceilf((mu.x - rr + 0.5f) * sx - 0.5f);
+    float xh = floorf((mu.x + rr + 0.5f) * sx - 0.5f);
+    float yl = ceilf((mu.y - rr + 0.5f) * sy - 0.5f);
+    float yh = floorf((mu.y + rr + 0.5f) * sy - 0.5f);
+    xl = fmaxf(xl, 0.0f); yl = fmaxf(yl, 0.0f);
+    xh = fminf(xh, (float)(oW - 1)); yh = fminf(yh, (float)(oH - 1));
+    int4 tb = make_int4(-1, -1, -1, -1);
+    if (ok && xl <= xh && yl <= yh) {
+        tb = make_int4((int)xl / TILE, (int)xh / TILE, (int)yl / TILE, (int)yh / TILE);
+        int y0 = max(tb.z, ty_lo), y1 = min(tb.w, ty_hi - 1);
+        for (int ty = y0; ty <= y1; ty++)
+            for (int tx = tb.x; tx <= tb.y; tx++) atomicAdd(&cnt[ty * nx + tx], 1);
+    }
+    tbox[k] = tb;
+}
+
+// ------------------------------------------------------------ a2 / a4 -----
+// Exclusive scan of the per-block counts (one CTA of 1024 threads, 4096
+// counts per round).  Produces start[n+1] and the scatter cursors, zeroes the
+// counts for the next binning, publishes P and latches overflow.  Also zeroes
+// the loss partials consumed by the raster that follows.
+__global__ void __launch_bounds__(1024)
+k_scan(int *__restrict__ cnt, int n, int *__restrict__ start, int *__restrict__ cursor,
+       long long cap, GridCtr *gc, double *dstats)
+{
+    __shared__ int warp_tot[32];
+    __shared__ long long carry_s;
+    int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) carry_s = 0;
+    if (tid < 4 && dstats) dstats[tid] = 0.0;
+    __syncthreads();
+    for (int base = 0; base < n; base += 4096) {
+        int i0 = base + tid * 4;
+        int v[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) v[q] = (i0 + q < n) ? cnt[i0 + q] : 0;
+        int loc = v[0] + v[1] + v[2] + v[3];
+        int incl = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) warp_tot[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            int w = warp_tot[lane];
+            int wi = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int t = __shfl_up_sync(FULL, wi, o);
+                if (lane >= o) wi += t;
+            }
+            warp_tot[lane] = wi - w;  // exclusive
+        }
+        __syncthreads();
+        long long carry = carry_s;
+        int ex = (int)carry + warp_tot[wid] + incl - loc;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            if (i0 + q < n) {
+                start[i0 + q] = ex;
+                cursor[i0 + q] = ex;
+                cnt[i0 + q] = 0;
+            }
+            ex += v[q];
+        }
+        __syncthreads();
+        if (tid == 1023) carry_s = carry + warp_tot[31] + incl;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        long long P = carry_s;
+        start[n] = (int)P;
+        gc->pairs = P;
+        if (P > cap) {
+            if (P > gc->need) gc->need = P;
+            gc->skipped += 1;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- a3 ------
+// First radix digit: every block b_n inside kernel k's box records k
+// ("Each intersected block b_n is recorded").
+__global__ void __launch_bounds__(256)
+k_scatter(int K, const int4 *__restrict__ tbox, int nx, int ty_lo, int ty_hi,
+          int *__restrict__ cursor, int *__restrict__ ids, long long cap, const GridCtr *gc)
+{
+    if (gc->pairs > cap) return;
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    int4 tb = tbox[k];
+    if (tb.x < 0) return;
+    int y0 = max(tb.z, ty_lo), y1 = min(tb.w, ty_hi - 1);
+    for (int ty = y0; ty <= y1; ty++)
+        for (int tx = tb.x; tx <= tb.y; tx++) {
+            int pos = atomicAdd(&cursor[ty * nx + tx], 1);
+            ids[pos] = k;
+        }
+}
+
+// ---------------------------------------------------------------- a4 ------
+// Second radix digit: sort each bucket by kernel id.  Buckets up to SORT_CAP
+// are bitonic-sorted in shared memory; larger ones are sorted in SORT_CAP
+// runs and merged in global memory (ids are unique, so the merge position of
+// an element is its index plus its rank in the other run).
+__device__ __forceinline__ void smem_bitonic(int *s, int np)
+{
+    for (int k = 2; k <= np; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < np; i += blockDim.x) {
+                int ixj = i ^ j;
+                if (ixj > i) {
+                    int a = s[i], b = s[ixj];
+                    bool asc = (i & k) == 0;
+                    if ((a > b) == asc) { s[i] = b; s[ixj] = a; }
+                }
+            }
+            __syncthreads();
+        }
+}
+
+__device__ __forceinline__ int lower_bound_i(const int *a, int n, int x)
+{
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        int m = (lo + hi) >> 1;
+        if (a[m] < x) lo = m + 1; else hi = m;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(256)
+k_sort_segs(const int *__restrict__ start, int *__restrict__ ids, int *__restrict__ tmp,
+            int tile0, long long cap, const GridCtr *gc)
+{
+    __shared__ int s[SORT_CAP];
+    if (gc->pairs > cap) return;
+    int t = tile0 + blockIdx.x;
+    int b = start[t], n = start[t + 1] - b;
+    if (n <= 1) return;
+    int *seg = ids + b;
+    for (int c0 = 0; c0 < n; c0 += SORT_CAP) {
+        int m = min(SORT_CAP, n - c0);
+        int np = 32;
+        while (np < m) np <<= 1;
+        for (int i = threadIdx.x; i < np; i += blockDim.x) s[i] = i < m ? seg[c0 + i] : 0x7fffffff;
+        __syncthreads();
+        smem_bitonic(s, np);
+        for (int i = threadIdx.x; i < m; i += blockDim.x) seg[c0 + i] = s[i];
+        __syncthreads();
+    }
+    if (n <= SORT_CAP) return;
+    int *src = seg, *dst = tmp + b;
+    for (int run = SORT_CAP; run < n; run <<= 1) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            int lo = (i / (2 * run)) * (2 * run);
+            int mid = min(lo + run, n), hi = min(lo + 2 * run, n);
+            int x = src[i];
+            int pos;
+            if (i < mid) pos = (i - lo) + lower_bound_i(src + mid, hi - mid, x);
+            else pos = (i - mid) + lower_bound_i(src + lo, mid - lo, x);
+            dst[lo + pos] = x;
+        }
+        __syncthreads();
+        int *sw = src; src = dst; dst = sw;
+    }
+    if (src != seg)
+        for (int i = threadIdx.x; i < n; i += blockDim.x) seg[i] = src[i];
+}
+
+// ------------------------------------------------------- a5 / a6 / a7 -----
+struct RasterArgs {
+    const float *rec;
+    const int *ids;
+    const int *start;
+    const GridCtr *gc;
+    long long cap;
+    int nx, tile0;
+    int oW, oH;
+    float sx, sy;        // source spacing of output samples: x = (j+1/2) sx - 1/2
+    float R2;
+    // training
+    const float *target; // [C][H][W] (H = oH, W = oW in training)
+    float e_scale;        // 2 / (H W C): dL/dy = e_scale (y - t)
+    float *acc;           // raw per-kernel sums [K][V]
+    double *dstats;       // SSE, clamped SSE, uncovered pixels
+    // render
+    float *out;           // [C][oH][oW]
+    // profiling (PROF instantiation only): tested / hit (pixel, kernel) pairs
+    unsigned long long *work;
+};
+
+// Multi-value warp reduction ("transpose" butterfly): V values per lane ->
+// lane holds the warp total of value idx(lane).  log2(V) exchange steps move
+// half of the remaining values each, then plain butterflies finish.
+template <int V>
+__device__ __forceinline__ float warp_reduce_transpose(float (&v)[V], int lane, int &idx)
+{
+    idx = 0;
+#pragma unroll
+    for (int n = V, off = 16; n > 1; n >>= 1, off >>= 1) {
+        bool up = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < n / 2; i++) {
+            float send = up ? v[i] : v[i + n / 2];
+            float keep = up ? v[i + n / 2] : v[i];
+            v[i] = keep + __shfl_xor_sync(FULL, send, off);
+        }
+        if (up) idx += n / 2;
+    }
+    constexpr int LOGV = V == 8 ? 3 : (V == 16 ? 4 : (V == 4 ? 2 : (V == 2 ? 1 : 5)));
+#pragma unroll
+    for (int off = 16 >> LOGV; off >= 1; off >>= 1) v[0] += __shfl_xor_sync(FULL, v[0], off);
+    return v[0];
+}
+
+// One CTA = one 16x16 block b_n, 128 threads = 4 warps, each warp an 8x8
+// quadrant, each lane a vertical pair of pixels.  The block's kernel list
+// K_n is staged through shared memory in batches; a warp skips a kernel when
+// none of its 64 pixels is inside the kernel's ellipse (warp-uniform branch).
+// TRAIN: forward sums D, N_c -> y -> loss partials -> backward sweep over K_n
+// with the per-pixel y, D kept in registers; per (warp, kernel) the raw
+// gradient sums are reduced across the warp and added with one vector of
+// atomics.  RENDER: forward only, y written to out.
+template <int C, int E, bool TRAIN, bool PROF>
+__global__ void __launch_bounds__(128)
+k_raster(RasterArgs A)
+{
+    using R = Rec<C, E>;
+    constexpr int RS4 = R::RS / 4;
+    constexpr int BATCH = 64;
+    __shared__ float4 srec[BATCH * RS4];
+    __shared__ int sid[BATCH];
+    __shared__ double red[3][4];
+    if (A.gc->pairs > A.cap) return;
+
+    const int tile = A.tile0 + blockIdx.x;
+    const int tx = tile % A.nx, ty = tile / A.nx;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int px = tx * TILE + (warp & 1) * 8 + (lane & 7);
+    const int py0 = ty * TILE + (warp >> 1) * 8 + (lane >> 3) * 2, py1 = py0 + 1;
+    const bool v0 = px < A.oW && py0 < A.oH, v1 = px < A.oW && py1 < A.oH;
+    const float xs = (px + 0.5f) * A.sx - 0.5f;
+    const float ys0 = (py0 + 0.5f) * A.sy - 0.5f, ys1 = (py1 + 0.5f) * A.sy - 0.5f;
+    const float R2 = A.R2;
+    const int s0 = A.start[tile], n = A.start[tile + 1] - s0;
+
+    float D0 = 0.f, D1 = 0.f, N0[C], N1[C];
+#pragma unroll
+    for (int c = 0; c < C; c++) N0[c] = N1[c] = 0.f;
+    unsigned long long w_tested = 0, w_hit = 0;
+    const int w_valid = PROF ? __popc(__ballot_sync(FULL, v0)) + __popc(__ballot_sync(FULL, v1)) : 0;
+
+    auto load_batch = [&](int b0, int nb) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < nb * RS4; i += blockDim.x) {
+            int j = i / RS4, q = i - j * RS4;
+            int id = A.ids[s0 + b0 + j];
+            srec[i] = reinterpret_cast<const float4 *>(A.rec)[(size_t)id * RS4 + q];
+            if (TRAIN && q == 0) sid[j] = id;
+        }
+        __syncthreads();
+    };
+
+    // ---- forward (Eq. 5 with the per-pixel cull of P:221) ----
+    for (int b0 = 0; b0 < n; b0 += BATCH) {
+        int nb = min(BATCH, n - b0);
+        load_batch(b0, nb);
+        for (int j = 0; j < nb; j++) {
+            float r[R::RS];
+#pragma unroll
+            for (int q = 0; q < RS4; q++) {
+                float4 f = srec[j * RS4 + q];
+                r[4 * q] = f.x; r[4 * q + 1] = f.y; r[4 * q + 2] = f.z; r[4 * q + 3] = f.w;
+            }
+            float dx = xs - r[0], dy0 = ys0 - r[1], dy1 = ys1 - r[1];
+            float u = r[2] * dx;
+            float w0 = fmaf(r[3], dx, r[4] * dy0), w1 = fmaf(r[3], dx, r[4] * dy1);
+            float uu = u * u;
+            float q0 = fmaf(w0, w0, uu), q1 = fmaf(w1, w1, uu);
+            bool h0 = v0 && q0 <= R2, h1 = v1 && q1 <= R2;
+            if (PROF) {
+                w_tested += w_valid;
+                w_hit += __popc(__ballot_sync(FULL, h0)) + __popc(__ballot_sync(FULL, h1));
+            }
+            if (!__any_sync(FULL, h0 || h1)) continue;
+            float g0 = h0 ? ex2_approx(fmaf(q0, -0.5f * LOG2E, r[5])) : 0.f;
+            float g1 = h1 ? ex2_approx(fmaf(q1, -0.5f * LOG2E, r[5])) : 0.f;
+            D0 += g0; D1 += g1;
+#pragma unroll
+            for (int c = 0; c < C; c++) {
+                float m0 = r[6 + c * E], m1 = m0;
+                if (E == 3) {
+                    m0 = fmaf(r[6 + c * E + 1], dx, fmaf(r[6 + c * E + 2], dy0, m0));
+                    m1 = fmaf(r[6 + c * E + 1], dx, fmaf(r[6 + c * E + 2], dy1, m1));
+                }
+                N0[c] = fmaf(g0, m0, N0[c]);
+                N1[c] = fmaf(g1, m1, N1[c]);
+            }
+        }
+    }
+    if (PROF && lane == 0) {
+        atomicAdd(&A.work[0], w_tested);
+        atomicAdd(&A.work[1], w_hit);
+    }
+    float y0[C], y1[C];
+    float iD0 = D0 > 0.f ? 1.0f / D0 : 0.f, iD1 = D1 > 0.f ? 1.0f / D1 : 0.f;
+#pragma unroll
+    for (int c = 0; c < C; c++) { y0[c] = N0[c] * iD0; y1[c] = N1[c] * iD1; }
+
+    if (!TRAIN) {
+        size_t plane = (size_t)A.oH * A.oW;
+#pragma unroll
+        for (int c = 0; c < C; c++) {
+            if (v0) A.out[c * plane + (size_t)py0 * A.oW + px] = y0[c];
+            if (v1) A.out[c * plane + (size_t)py1 * A.oW + px] = y1[c];
+        }
+        return;
+    }
+
+    // ---- loss / PSNR partials (Q8) and per-pixel backward seeds ----
+    float eD0[C], eD1[C], K0 = 0.f, K1 = 0.f;
+    double sse = 0.0, ssec = 0.0, unc = 0.0;
+    {
+        size_t plane = (size_t)A.oH * A.oW;
+#pragma unroll
+        for (int c = 0; c < C; c++) {
+            float t0 = v0 ? A.target[c * plane + (size_t)py0 * A.oW + px] : 0.f;
+            float t1 = v1 ? A.target[c * plane + (size_t)py1 * A.oW + px] : 0.f;
+            float r0 = v0 ? y0[c] - t0 : 0.f, r1 = v1 ? y1[c] - t1 : 0.f;
+            float rc0 = v0 ? __saturatef(y0[c]) - __saturatef(t0) : 0.f;
+            float rc1 = v1 ? __saturatef(y1[c]) - __saturatef(t1) : 0.f;
+            sse += (double)(r0 * r0) + (double)(r1 * r1);
+            ssec += (double)(rc0 * rc0) + (double)(rc1 * rc1);
+            eD0[c] = A.e_scale * r0 * iD0;      // dL/dy_c / D  (0 if uncovered)
+            eD1[c] = A.e_scale * r1 * iD1;
+            K0 = fmaf(eD0[c], y0[c], K0);
+            K1 = fmaf(eD1[c], y1[c], K1);
+        }
+        unc = (double)((v0 && D0 <= 0.f) ? 1 : 0) + (double)((v1 && D1 <= 0.f) ? 1 : 0);
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            sse += __shfl_xor_sync(FULL, sse, o);
+            ssec += __shfl_xor_sync(FULL, ssec, o);
+            unc += __shfl_xor_sync(FULL, unc, o);
+        }
+        if (lane == 0) { red[0][warp] = sse; red[1][warp] = ssec; red[2][warp] = unc; }
+        __syncthreads();
+        if (threadIdx.x < 3) {
+            double s = red[threadIdx.x][0] + red[threadIdx.x][1] + red[threadIdx.x][2] + red[threadIdx.x][3];
+            if (s != 0.0) atomicAdd(&A.dstats[threadIdx.x], s);
+        }
+    }
+
+    // ---- backward (appendix of DESIGN.md: raw sums per kernel) ----
+    // s = dL/d(d^2) = -1/2 g G,  G = sum_c eD_c m_c(x) - sum_c eD_c y_c
+    // raw: Su, Sv, Sux(=sum s u dx), Svx, Svy, Ss, then per channel
+    // sum g eD_c (, sum g eD_c dx, sum g eD_c dy)
+    for (int b0 = 0; b0 < n; b0 += BATCH) {
+        int nb = min(BATCH, n - b0);
+        if (n > BATCH) load_batch(b0, nb);   // n <= BATCH: batch 0 is still resident
+        for (int j = 0; j < nb; j++) {
+            float r[R::RS];
+#pragma unroll
+            for (int q = 0; q < RS4; q++) {
+                float4 f = srec[j * RS4 + q];
+                r[4 * q] = f.x; r[4 * q + 1] = f.y; r[4 * q + 2] = f.z; r[4 * q + 3] = f.w;
+            }
+            float dx = xs - r[0], dy0 = ys0 - r[1], dy1 = ys1 - r[1];
+            float u = r[2] * dx;
+            float w0 = fmaf(r[3], dx, r[4] * dy0), w1 = fmaf(r[3], dx, r[4] * dy1);
+            float uu = u * u;
+            float q0 = fmaf(w0, w0, uu), q1 = fmaf(w1, w1, uu);
+            bool h0 = v0 && q0 <= R2 && D0 > 0.f, h1 = v1 && q1 <= R2 && D1 > 0.f;
+            if (!__any_sync(FULL, h0 || h1)) continue;
+            float g0 = h0 ? ex2_approx(fmaf(q0, -0.5f * LOG2E, r[5])) : 0.f;
+            float g1 = h1 ? ex2_approx(fmaf(q1, -0.5f * LOG2E, r[5])) : 0.f;
+            float G0 = -K0, G1 = -K1;
+            float acc[R::V];
+#pragma unroll
+            for (int c = 0; c < C; c++) {
+                float m0 = r[6 + c * E], m1 = m0;
+                if (E == 3) {
+                    m0 = fmaf(r[6 + c * E + 1], dx, fmaf(r[6 + c * E + 2], dy0, m0));
+                    m1 = fmaf(r[6 + c * E + 1], dx, fmaf(r[6 + c * E + 2], dy1, m1));
+                }
+                G0 = fmaf(eD0[c], m0, G0);
+                G1 = fmaf(eD1[c], m1, G1);
+                float ge0 = g0 * eD0[c], ge1 = g1 * eD1[c];
+                acc[6 + c * E] = ge0 + ge1;
+                if (E == 3) {
+                    acc[6 + c * E + 1] = (ge0 + ge1) * dx;
+                    acc[6 + c * E + 2] = fmaf(ge0, dy0, ge1 * dy1);
+                }
+            }
+            float sa = -0.5f * g0 * G0, sb = -0.5f * g1 * G1;
+            float sv = fmaf(sa, w0, sb * w1);
+            acc[0] = (sa + sb) * u;
+            acc[1] = sv;
+            acc[2] = (sa + sb) * u * dx;
+            acc[3] = sv * dx;
+            acc[4] = fmaf(sa * w0, dy0, sb * w1 * dy1);
+            acc[5] = sa + sb;
+#pragma unroll
+            for (int i = R::P; i < R::V; i++) acc[i] = 0.f;
+            int idx;
+            float tot = warp_reduce_transpose<R::V>(acc, lane, idx);
+            constexpr int GROUP = 32 / R::V;   // lanes sharing one value index
+            if ((lane & (GROUP - 1)) == 0 && idx < R::P)
+                atomicAdd(&A.acc[(size_t)sid[j] * R::V + idx], tot);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- a8 ------
+// MODE 0 (step):   raw sums -> parameter gradients -> Adam -> clamp; reset sums
+// MODE 1 (grad):   raw sums -> parameter gradients -> grad_out; reset sums
+// MODE 2 (apply):  grad_in -> Adam -> clamp
+// Chain rule (DESIGN.md appendix A): with raw Su, Sv, Sux, Svx, Svy, Ss, gm,
+//   dL/dmu_x = -2 (a Su + b Sv) - sum_c Wx_c gm_c
+//   dL/dmu_y = -2 c Sv          - sum_c Wy_c gm_c
+//   dL/dl11  = -2 (a^2 Sux + a b Svx)
+//   dL/dl21  = -2 a c Svx
+//   dL/dl22  = -2 (b c Svx + c^2 Svy)
+//   dL/dlog_pi = -2 Ss
+// Adam (Q9): beta1 0.9, beta2 0.999, eps 1e-8 outside the sqrt,
+// bias-corrected; clamp l11, l22 >= 1e-3.  Moments are stored
+// parameter-major m[Pk][K] so every access is coalesced.
+template <int C, int E, int MODE>
+__global__ void __launch_bounds__(256)
+k_adam(int K, ParamsMut p, float *__restrict__ acc, const float *__restrict__ grad_in,
+       float *__restrict__ grad_out, float *__restrict__ m1, float *__restrict__ m2,
+       LrDev lr, HandleCtr *hc, const GridCtr *gc, long long cap)
+{
+    using R = Rec<C, E>;
+    constexpr int P = R::P;
+    if (MODE != 2 && gc->pairs > cap) return;
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    float g[P];
+    float mu_x = 0.f, mu_y = 0.f, l11 = 0.f, l21 = 0.f, l22 = 0.f;
+    bool live = k < K;
+    if (live) {
+        mu_x = p.mu[2 * k]; mu_y = p.mu[2 * k + 1];
+        l11 = p.chol[3 * k]; l21 = p.chol[3 * k + 1]; l22 = p.chol[3 * k + 2];
+        if (MODE == 2) {
+#pragma unroll
+            for (int i = 0; i < P; i++) g[i] = grad_in[(size_t)k * P + i];
+        } else {
+            float raw[R::V];
+            float4 *ap = reinterpret_cast<float4 *>(acc) + (size_t)k * (R::V / 4);
+#pragma unroll
+            for (int q = 0; q < R::V / 4; q++) {
+                float4 f = ap[q];
+                raw[4 * q] = f.x; raw[4 * q + 1] = f.y; raw[4 * q + 2] = f.z; raw[4 * q + 3] = f.w;
+                ap[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            float a = 1.0f / l11, c = 1.0f / l22;
+            float b = -l21 / (l11 * l22);
+            float ex_x = 0.f, ex_y = 0.f;
+            if (E == 3) {
+#pragma unroll
+                for (int ch = 0; ch < C; ch++) {
+                    ex_x = fmaf(p.expert[(size_t)k * C * E + ch * E + 1], raw[6 + ch * E], ex_x);
+                    ex_y = fmaf(p.expert[(size_t)k * C * E + ch * E + 2], raw[6 + ch * E], ex_y);
+                }
+            }
+            g[0] = -2.f * fmaf(a, raw[0], b * raw[1]) - ex_x;
+            g[1] = -2.f * c * raw[1] - ex_y;
+            g[2] = -2.f * fmaf(a * a, raw[2], a * b * raw[3]);
+            g[3] = -2.f * a * c * raw[3];
+            g[4] = -2.f * fmaf(b * c, raw[3], c * c * raw[4]);
+            g[5] = -2.f * raw[5];
+#pragma unroll
+            for (int i = 6; i < P; i++) g[i] = raw[i];
+        }
+        bool ok = true;
+#pragma unroll
+        for (int i = 0; i < P; i++) ok = ok && isfinite(g[i]);
+        if (!ok) atomicExch((unsigned long long *)&hc->nonfinite, 1ull);
+    }
+    if (MODE == 1) {
+        if (live) {
+#pragma unroll
+            for (int i = 0; i < P; i++) grad_out[(size_t)k * P + i] = g[i];
+        }
+        return;
+    }
+    long long t = hc->t + 1;
+    if (live) {
+        const float b1 = 0.9f, b2 = 0.999f, eps = 1e-8f;
+        float bc1 = (float)(1.0 - pow(0.9, (double)t));
+        float bc2 = (float)(1.0 - pow(0.999, (double)t));
+        float prm[P];
+        prm[0] = mu_x; prm[1] = mu_y; prm[2] = l11; prm[3] = l21; prm[4] = l22;
+        prm[5] = p.log_pi[k];
+#pragma unroll
+        for (int i = 6; i < P; i++) prm[i] = p.expert[(size_t)k * C * E + (i - 6)];
+#pragma unroll
+        for (int i = 0; i < P; i++) {
+            float lri = i < 2 ? lr.mu : (i < 5 ? lr.chol : (i == 5 ? lr.log_pi : (((i - 6) % E) == 0 ? lr.expert : lr.slope)));
+            size_t o = (size_t)i * K + k;
+            float a1 = fmaf(b1, m1[o], (1.f - b1) * g[i]);
+            float a2 = fmaf(b2, m2[o], (1.f - b2) * g[i] * g[i]);
+            m1[o] = a1; m2[o] = a2;
+            prm[i] -= lri * (a1 / bc1) / (sqrtf(a2 / bc2) + eps);
+        }
+        prm[2] = fmaxf(prm[2], 1e-3f);
+        prm[4] = fmaxf(prm[4], 1e-3f);
+        p.mu[2 * k] = prm[0]; p.mu[2 * k + 1] = prm[1];
+        p.chol[3 * k] = prm[2]; p.chol[3 * k + 1] = prm[3]; p.chol[3 * k + 2] = prm[4];
+        p.log_pi[k] = prm[5];
+#pragma unroll
+        for (int i = 6; i < P; i++) p.expert[(size_t)k * C * E + (i - 6)] = prm[i];
+    }
+    // last CTA advances the step counter after every CTA has read it
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        unsigned int ticket = atomicAdd(&hc->done, 1u);
+        if (ticket == gridDim.x - 1) {
+            hc->t = t;
+            hc->done = 0;
+            __threadfence();
+        }
+    }
+}
+
+}  // namespace smoe

@@ -1,0 +1,350 @@
+"""Thin Python binding of the C-ABI library ``libsmoe.so`` (include/smoe.h).
+
+Argument marshalling only: every step of the hot path runs in the CUDA
+kernels behind the ABI.  PyTorch provides device memory and streams.  There
+is no fallback: if ``libsmoe.so`` is missing or no CUDA device is present the
+calls fail loudly.
+
+The function names mirror the C entry points (``smoe_create``, ``smoe_step``,
+``smoe_render``, ...); :class:`SMoE` wraps a handle with the same methods.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsmoe.so")
+_LIB = None
+
+OK, ERR_INVALID_ARG, ERR_CUDA, ERR_OUT_OF_MEMORY, ERR_NONFINITE, ERR_CAPACITY, ERR_BAD_HANDLE = range(7)
+
+
+class SmoeError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"[{status}] {msg}")
+        self.status = status
+
+
+class c_params(ctypes.Structure):
+    _fields_ = [("mu", ctypes.c_void_p), ("chol", ctypes.c_void_p),
+                ("log_pi", ctypes.c_void_p), ("expert", ctypes.c_void_p)]
+
+
+class c_lr(ctypes.Structure):
+    _fields_ = [("mu", ctypes.c_float), ("chol", ctypes.c_float), ("log_pi", ctypes.c_float),
+                ("expert", ctypes.c_float), ("slope", ctypes.c_float)]
+
+
+class c_stats(ctypes.Structure):
+    _fields_ = [("loss", ctypes.c_double), ("psnr_db", ctypes.c_double), ("sse", ctypes.c_double),
+                ("sse_clamped", ctypes.c_double), ("pairs", ctypes.c_longlong),
+                ("uncovered_px", ctypes.c_longlong), ("n_tiles", ctypes.c_longlong)]
+
+
+class c_kernel_time(ctypes.Structure):
+    _fields_ = [("total_ms", ctypes.c_double), ("launches", ctypes.c_longlong)]
+
+
+class c_work(ctypes.Structure):
+    _fields_ = [("tested_pairs", ctypes.c_longlong), ("hit_pairs", ctypes.c_longlong)]
+
+
+KERNEL_COUNT = 7
+
+
+class c_options(ctypes.Structure):
+    _fields_ = [("K", ctypes.c_int), ("H", ctypes.c_int), ("W", ctypes.c_int), ("C", ctypes.c_int),
+                ("expert_order", ctypes.c_int), ("R2", ctypes.c_double), ("device", ctypes.c_int),
+                ("pair_capacity", ctypes.c_longlong)]
+
+
+def lib():
+    """Load libsmoe.so (fails loudly when the extension was not built)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: build the CUDA extension (python -c "
+                          "'import __graft_entry__ as g; g.build()')")
+    L = ctypes.CDLL(LIB_PATH)
+    H = ctypes.c_void_p
+    P = ctypes.c_void_p
+    I = ctypes.c_int
+    st = ctypes.c_int
+    sig = {
+        "smoe_default_options": (st, [ctypes.POINTER(c_options)]),
+        "smoe_create": (st, [I, I, I, I, I, ctypes.POINTER(H)]),
+        "smoe_create_ex": (st, [ctypes.POINTER(c_options), ctypes.POINTER(H)]),
+        "smoe_destroy": (st, [H]),
+        "smoe_set_stream": (st, [H, P]),
+        "smoe_render": (st, [H, ctypes.POINTER(c_params), I, I, P]),
+        "smoe_step": (st, [H, ctypes.POINTER(c_params), P, ctypes.POINTER(c_lr), ctypes.POINTER(c_stats)]),
+        "smoe_set_band": (st, [H, I, I]),
+        "smoe_grad": (st, [H, ctypes.POINTER(c_params), P, P, P]),
+        "smoe_apply": (st, [H, ctypes.POINTER(c_params), P, ctypes.POINTER(c_lr)]),
+        "smoe_reset_adam": (st, [H]),
+        "smoe_sync": (st, [H, ctypes.POINTER(c_stats)]),
+        "smoe_bin": (st, [H, ctypes.POINTER(c_params), I, I, P, P, ctypes.c_longlong,
+                          ctypes.POINTER(ctypes.c_longlong), P]),
+        "smoe_paper_lr": (c_lr, [I, I]),
+        "smoe_launch_count": (ctypes.c_longlong, [H]),
+        "smoe_profile_begin": (st, [H, I]),
+        "smoe_profile_end": (st, [H, P, ctypes.POINTER(c_work)]),
+        "smoe_kernel_name": (ctypes.c_char_p, [I]),
+        "smoe_status_string": (ctypes.c_char_p, [st]),
+        "smoe_last_error": (ctypes.c_char_p, [H]),
+        "smoe_abi_version": (I, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _LIB = L
+    return L
+
+
+def _check(status: int, handle=None):
+    if status != OK:
+        msg = lib().smoe_last_error(handle).decode(errors="replace")
+        raise SmoeError(status, msg or lib().smoe_status_string(status).decode())
+
+
+@dataclass
+class Params:
+    """Kernel parameters as float32 CUDA tensors in the ABI layout:
+    mu[K,2], chol[K,3] = (l11, l21, l22), log_pi[K], expert[K,C,E]."""
+    mu: torch.Tensor
+    chol: torch.Tensor
+    log_pi: torch.Tensor
+    expert: torch.Tensor
+
+    @staticmethod
+    def from_numpy(pool, device="cuda") -> "Params":
+        t = lambda a: torch.as_tensor(a, dtype=torch.float32).contiguous().to(device)
+        return Params(t(pool.mu), t(pool.chol), t(pool.log_pi), t(pool.expert))
+
+    def clone(self) -> "Params":
+        return Params(self.mu.clone(), self.chol.clone(), self.log_pi.clone(), self.expert.clone())
+
+    def flat(self) -> torch.Tensor:
+        K = self.mu.shape[0]
+        return torch.cat([self.mu, self.chol, self.log_pi[:, None], self.expert.reshape(K, -1)], 1)
+
+    def c(self) -> c_params:
+        for t in (self.mu, self.chol, self.log_pi, self.expert):
+            if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+                raise SmoeError(ERR_INVALID_ARG, "params must be contiguous float32 CUDA tensors")
+        return c_params(self.mu.data_ptr(), self.chol.data_ptr(), self.log_pi.data_ptr(),
+                        self.expert.data_ptr())
+
+
+@dataclass
+class LR:
+    """Per-group learning rates of one step (readings Q11, Q13)."""
+    mu: float = 0.01
+    chol: float = 1e-3
+    log_pi: float = 0.0
+    expert: float = 1e-3
+    slope: float = 2e-4
+
+    def c(self) -> c_lr:
+        return c_lr(self.mu, self.chol, self.log_pi, self.expert, self.slope)
+
+    @staticmethod
+    def paper(t: int, T: int) -> "LR":
+        l = lib().smoe_paper_lr(int(t), int(T))
+        return LR(l.mu, l.chol, l.log_pi, l.expert, l.slope)
+
+
+@dataclass
+class Stats:
+    loss: float
+    psnr_db: float
+    sse: float
+    sse_clamped: float
+    pairs: int
+    uncovered_px: int
+    n_tiles: int
+
+    @staticmethod
+    def of(s: c_stats) -> "Stats":
+        return Stats(s.loss, s.psnr_db, s.sse, s.sse_clamped, s.pairs, s.uncovered_px, s.n_tiles)
+
+
+def _ptr(x):
+    """Raw address of a contiguous torch tensor or numpy array (host or device)."""
+    if x is None:
+        return None
+    if isinstance(x, torch.Tensor):
+        if not x.is_contiguous():
+            raise SmoeError(ERR_INVALID_ARG, "buffers must be contiguous")
+        return x.data_ptr()
+    if hasattr(x, "ctypes") and hasattr(x, "flags"):
+        if not x.flags["C_CONTIGUOUS"]:
+            raise SmoeError(ERR_INVALID_ARG, "buffers must be contiguous")
+        return x.ctypes.data
+    return x
+
+
+class SMoE:
+    """A library handle: K kernels fitting an H x W x C image with constant
+    (order 0) or linear (order 1) experts (B.json smoe_create)."""
+
+    def __init__(self, K: int, H: int, W: int, C: int, expert_order: int = 0, R2: float | None = None,
+                 device: int | None = None, pair_capacity: int = 0):
+        L = lib()
+        o = c_options()
+        _check(L.smoe_default_options(ctypes.byref(o)))
+        o.K, o.H, o.W, o.C, o.expert_order = K, H, W, C, expert_order
+        if R2 is not None:
+            o.R2 = R2
+        o.device = torch.cuda.current_device() if device is None else device
+        o.pair_capacity = pair_capacity
+        h = ctypes.c_void_p()
+        _check(L.smoe_create_ex(ctypes.byref(o), ctypes.byref(h)))
+        self.h = h
+        self.K, self.H, self.W, self.C, self.order = K, H, W, C, expert_order
+        self.E = 1 + 2 * expert_order
+        self.Pk = 6 + C * self.E
+        self.device = o.device
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().smoe_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _stream(self):
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        _check(lib().smoe_set_stream(self.h, ctypes.c_void_p(s)), self.h)
+
+    def step(self, params: Params, target, lr: LR | None = None, stats: bool = True):
+        """smoe_step: one fit iteration in place on ``params``; returns the
+        pre-update Stats when ``stats`` (synchronising), else None."""
+        self._stream()
+        lr = lr or LR()
+        p = params.c()
+        if stats:
+            s = c_stats()
+            _check(lib().smoe_step(self.h, ctypes.byref(p), _ptr(target), ctypes.byref(lr.c()),
+                                   ctypes.byref(s)), self.h)
+            return Stats.of(s)
+        _check(lib().smoe_step(self.h, ctypes.byref(p), _ptr(target), ctypes.byref(lr.c()), None), self.h)
+        return None
+
+    def render(self, params: Params, out_H: int | None = None, out_W: int | None = None, out=None):
+        """smoe_render: y on an out_H x out_W raster -> [C, out_H, out_W]."""
+        self._stream()
+        out_H = self.H if out_H is None else out_H
+        out_W = self.W if out_W is None else out_W
+        if out is None:
+            out = torch.empty((self.C, out_H, out_W), dtype=torch.float32, device=f"cuda:{self.device}")
+        _check(lib().smoe_render(self.h, ctypes.byref(params.c()), out_H, out_W, _ptr(out)), self.h)
+        return out
+
+    def set_band(self, tile_row0: int, tile_row1: int):
+        _check(lib().smoe_set_band(self.h, tile_row0, tile_row1), self.h)
+
+    def grad(self, params: Params, target, grad=None, sums=None):
+        """smoe_grad: (grad[K,Pk], sums[3] = SSE, clamped SSE, uncovered)."""
+        self._stream()
+        dev = f"cuda:{self.device}"
+        if grad is None:
+            grad = torch.empty((self.K, self.Pk), dtype=torch.float32, device=dev)
+        if sums is None:
+            sums = torch.empty(3, dtype=torch.float64, device=dev)
+        _check(lib().smoe_grad(self.h, ctypes.byref(params.c()), _ptr(target), _ptr(grad), _ptr(sums)), self.h)
+        return grad, sums
+
+    def apply(self, params: Params, grad, lr: LR | None = None):
+        self._stream()
+        _check(lib().smoe_apply(self.h, ctypes.byref(params.c()), _ptr(grad), ctypes.byref((lr or LR()).c())),
+               self.h)
+
+    def reset_adam(self):
+        _check(lib().smoe_reset_adam(self.h), self.h)
+
+    def sync(self) -> Stats:
+        s = c_stats()
+        _check(lib().smoe_sync(self.h, ctypes.byref(s)), self.h)
+        return Stats.of(s)
+
+    def bin(self, params: Params, out_H: int | None = None, out_W: int | None = None):
+        """smoe_bin: (tile_range[n_tiles+1], ids[P], tilebox[K,4]) as int64 CPU tensors."""
+        self._stream()
+        out_H = self.H if out_H is None else out_H
+        out_W = self.W if out_W is None else out_W
+        nt = ((out_H + 15) // 16) * ((out_W + 15) // 16)
+        rng = torch.empty(nt + 1, dtype=torch.int32)
+        tb = torch.empty((self.K, 4), dtype=torch.int32)
+        n = ctypes.c_longlong()
+        _check(lib().smoe_bin(self.h, ctypes.byref(params.c()), out_H, out_W, rng.data_ptr(), None, 0,
+                              ctypes.byref(n), tb.data_ptr()), self.h)
+        ids = torch.empty(max(1, n.value), dtype=torch.int32)
+        _check(lib().smoe_bin(self.h, ctypes.byref(params.c()), out_H, out_W, rng.data_ptr(), ids.data_ptr(),
+                              ids.numel(), ctypes.byref(n), tb.data_ptr()), self.h)
+        return rng.long(), ids[:n.value].long(), tb.long()
+
+    def launch_count(self) -> int:
+        return int(lib().smoe_launch_count(self.h))
+
+    def profile_begin(self, max_launches: int):
+        """smoe_profile_begin: time the next launches with CUDA events."""
+        _check(lib().smoe_profile_begin(self.h, int(max_launches)), self.h)
+
+    def profile_end(self):
+        """smoe_profile_end -> ({kernel name: (total_ms, launches)}, (tested, hit))."""
+        arr = (c_kernel_time * KERNEL_COUNT)()
+        w = c_work()
+        _check(lib().smoe_profile_end(self.h, ctypes.cast(arr, ctypes.c_void_p), ctypes.byref(w)), self.h)
+        out = {}
+        for i in range(KERNEL_COUNT):
+            if arr[i].launches:
+                out[lib().smoe_kernel_name(i).decode()] = (arr[i].total_ms, arr[i].launches)
+        return out, (w.tested_pairs, w.hit_pairs)
+
+
+# C-named module-level wrappers (the binding keeps the ABI's names).
+def smoe_create(K, H, W, C, expert_order=0, **kw) -> SMoE:
+    return SMoE(K, H, W, C, expert_order, **kw)
+
+
+def smoe_step(h: SMoE, params, target, lr=None, stats=True):
+    return h.step(params, target, lr, stats)
+
+
+def smoe_render(h: SMoE, params, out_H=None, out_W=None, out=None):
+    return h.render(params, out_H, out_W, out)
+
+
+def smoe_grad(h: SMoE, params, target, grad=None, sums=None):
+    return h.grad(params, target, grad, sums)
+
+
+def smoe_apply(h: SMoE, params, grad, lr=None):
+    return h.apply(params, grad, lr)
+
+
+def smoe_set_band(h: SMoE, r0, r1):
+    return h.set_band(r0, r1)
+
+
+def smoe_sync(h: SMoE):
+    return h.sync()
+
+
+def smoe_bin(h: SMoE, params, out_H=None, out_W=None):
+    return h.bin(params, out_H, out_W)
+
+
+def smoe_destroy(h: SMoE):
+    h.close()

@@ -1,0 +1,333 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded, margin-conditioned inputs (rule P1).
+
+Bars (BASELINE.json north_star):
+  * block ranges and sort order bit-exact;
+  * pixels |dy| <= 1e-5 |y| + 1e-6;
+  * gradients |dg| <= 1e-4 |g| + 1e-5 A_ref;
+  * PSNR after a 100-iteration fit within 0.01 dB.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_2510_05814_b200 import smoe, synth
+from helpers import assert_grads, assert_pixels, conditioned, conditioned_multi
+
+pytestmark = pytest.mark.gpu
+
+
+def dev_pool(pool):
+    return smoe.Params.from_numpy(pool, "cuda")
+
+
+def opar(pool):
+    return O.Params.from_any(pool)
+
+
+# ----------------------------------------------------------- binning a1-a4 --
+
+BIN_CASES = [
+    # H, W, C, K, order, out scale, seed
+    (37, 53, 1, 40, 0, 1.0, 1),
+    (37, 53, 3, 40, 1, 2.0, 2),
+    (64, 48, 3, 120, 0, 0.5, 3),
+    (50, 70, 1, 90, 0, 1.5, 4),
+    (130, 97, 3, 600, 1, 1.0, 5),
+]
+
+
+@pytest.mark.parametrize("H,W,C,K,order,scale,seed", BIN_CASES)
+def test_binning_bit_exact(H, W, C, K, order, scale, seed):
+    oH, oW = int(round(H * scale)), int(round(W * scale))
+    pool = synth.aniso_pool(H, W, C, K, seed, order=order, margin_px=8)
+    pool = conditioned(pool, H, W, oH, oW)
+    h = smoe.SMoE(K, H, W, C, order)
+    rng, ids, tb = h.bin(dev_pool(pool), oH, oW)
+    _, tb_ref, _ = O.boxes(opar(pool), H, W, oH, oW)
+    nx, ny = -(-oW // 16), -(-oH // 16)
+    rng_ref, ids_ref = O.tile_list(tb_ref, nx, ny)
+    np.testing.assert_array_equal(tb.numpy(), tb_ref)
+    np.testing.assert_array_equal(rng.numpy(), rng_ref)
+    np.testing.assert_array_equal(ids.numpy(), ids_ref)
+
+
+def test_binning_kodak_density_and_determinism():
+    """768x512 Kodak-shaped, 10k paper-init kernels (config 2 geometry)."""
+    H, W = 512, 768
+    img = synth.image(H, W, 3, 1236)
+    pool = conditioned(synth.paper_init(img, 10_000, 1237, order=1), H, W)
+    h = smoe.SMoE(10_000, H, W, 3, 1)
+    p = dev_pool(pool)
+    rng, ids, tb = h.bin(p)
+    _, tb_ref, _ = O.boxes(opar(pool), H, W)
+    rng_ref, ids_ref = O.tile_list(tb_ref, 48, 32)
+    np.testing.assert_array_equal(rng.numpy(), rng_ref)
+    np.testing.assert_array_equal(ids.numpy(), ids_ref)
+    rng2, ids2, _ = h.bin(p)
+    np.testing.assert_array_equal(ids2.numpy(), ids.numpy())
+    avg = len(ids_ref) / (48 * 32)
+    assert 40 < avg < 70   # ~52.9 at the sigma=5 init; paper: 51 at Kodak/10k
+
+
+def test_binning_large_bucket_merge_path():
+    """A bucket larger than the in-smem sort capacity (2048) exercises the
+    global merge; all kernels sit inside one 16x16 block."""
+    H, W, K = 32, 32, 5000
+    g = np.random.default_rng(0)
+    pool = synth.aniso_pool(H, W, 1, K, 9, l_range=(0.3, 0.6), shear=0.1)
+    pool.mu[:] = g.uniform(18.2, 29.8, (K, 2)).astype(np.float32)
+    pool = conditioned(pool, H, W)
+    h = smoe.SMoE(K, H, W, 1, 0)
+    rng, ids, _ = h.bin(dev_pool(pool))
+    _, tb_ref, _ = O.boxes(opar(pool), H, W)
+    rng_ref, ids_ref = O.tile_list(tb_ref, 2, 2)
+    assert (rng_ref[1:] - rng_ref[:-1]).max() > 2048
+    np.testing.assert_array_equal(rng.numpy(), rng_ref)
+    np.testing.assert_array_equal(ids.numpy(), ids_ref)
+
+
+def test_binning_empty_and_outside():
+    H, W = 40, 40
+    pool = synth.aniso_pool(H, W, 1, 10, 3)
+    pool.mu[:, 0] += 500.0          # every kernel far outside the image
+    h = smoe.SMoE(10, H, W, 1, 0)
+    rng, ids, tb = h.bin(dev_pool(pool))
+    assert ids.numel() == 0 and int(rng[-1]) == 0
+    assert (tb == -1).all()
+    y = h.render(dev_pool(pool))
+    assert float(y.abs().max()) == 0.0        # Q7: uncovered pixels render 0
+
+
+# ------------------------------------------------------------- render a5/a9 --
+
+RENDER_CASES = [
+    (37, 53, 1, 40, 0, 1.0),
+    (37, 53, 3, 40, 1, 1.0),
+    (64, 48, 3, 120, 0, 2.0),
+    (33, 47, 3, 60, 1, 4.0),
+    (64, 80, 1, 150, 1, 0.5),
+    (48, 40, 3, 90, 0, 1.5),
+]
+
+
+@pytest.mark.parametrize("H,W,C,K,order,scale", RENDER_CASES)
+def test_render_parity(H, W, C, K, order, scale):
+    oH, oW = int(round(H * scale)), int(round(W * scale))
+    pool = synth.aniso_pool(H, W, C, K, 10 + K, order=order, margin_px=6, log_pi_sd=0.5)
+    pool = conditioned(pool, H, W, oH, oW)
+    h = smoe.SMoE(K, H, W, C, order)
+    y = h.render(dev_pool(pool), oH, oW).cpu().numpy()
+    y_ref, D_ref = O.render(opar(pool), H, W, oH, oW)
+    assert (D_ref > 0).mean() > 0.5
+    assert_pixels(y, y_ref)
+    # deterministic: the forward has no atomics
+    y2 = h.render(dev_pool(pool), oH, oW).cpu().numpy()
+    np.testing.assert_array_equal(y, y2)
+
+
+def test_render_host_output_buffer():
+    H, W, C, K = 30, 30, 3, 30
+    pool = conditioned(synth.aniso_pool(H, W, C, K, 77), H, W)
+    h = smoe.SMoE(K, H, W, C, 0)
+    out = torch.empty((C, H, W), dtype=torch.float32).pin_memory()
+    h.render(dev_pool(pool), H, W, out=out)
+    y_ref, _ = O.render(opar(pool), H, W)
+    assert_pixels(out.numpy(), y_ref)
+
+
+# ------------------------------------------------------ loss + grads a6/a7 --
+
+GRAD_CASES = [
+    (37, 53, 1, 40, 0),
+    (37, 53, 3, 40, 0),
+    (40, 36, 3, 50, 1),
+    (64, 64, 1, 64, 1),
+    (70, 45, 3, 140, 1),
+]
+
+
+@pytest.mark.parametrize("H,W,C,K,order", GRAD_CASES)
+def test_grad_parity(H, W, C, K, order):
+    pool = synth.aniso_pool(H, W, C, K, 30 + K, order=order, margin_px=5, log_pi_sd=0.4)
+    pool = conditioned(pool, H, W)
+    target = synth.image(H, W, C, 31 + K)
+    h = smoe.SMoE(K, H, W, C, order)
+    g, sums = h.grad(dev_pool(pool), torch.as_tensor(target).cuda())
+    lg = O.loss_grad(opar(pool), target.astype(np.float64))
+    s = sums.cpu().numpy()
+    assert abs(s[0] - lg.sse) <= 1e-5 * lg.sse
+    assert abs(s[1] - lg.sse_clamped) <= 1e-5 * lg.sse_clamped
+    assert int(s[2]) == lg.uncovered
+    assert_grads(g.cpu().numpy(), lg.grad, lg.grad_abs)
+
+
+def test_grad_host_buffers_and_uncovered():
+    H, W, C, K = 48, 48, 3, 12
+    pool = conditioned(synth.aniso_pool(H, W, C, K, 5, order=1), H, W)
+    target = synth.image(H, W, C, 6)
+    h = smoe.SMoE(K, H, W, C, 1)
+    g = np.zeros((K, h.Pk), np.float32)
+    sums = np.zeros(3)
+    h.grad(dev_pool(pool), target, grad=g, sums=sums)   # host target, grad, sums
+    lg = O.loss_grad(opar(pool), target.astype(np.float64))
+    assert lg.uncovered > 0 and int(sums[2]) == lg.uncovered
+    assert_grads(g, lg.grad, lg.grad_abs)
+
+
+def test_band_additivity_on_one_gpu():
+    """Per-band gradients (multi-GPU tile-row bands) add up to the full one."""
+    H, W, C, K = 80, 64, 3, 150
+    pool = conditioned(synth.aniso_pool(H, W, C, K, 41, order=1), H, W)
+    target = torch.as_tensor(synth.image(H, W, C, 42)).cuda()
+    h = smoe.SMoE(K, H, W, C, 1)
+    p = dev_pool(pool)
+    full, fs = h.grad(p, target)
+    acc = torch.zeros_like(full)
+    sacc = torch.zeros_like(fs)
+    for r0, r1 in [(0, 2), (2, 3), (3, 5)]:
+        h.set_band(r0, r1)
+        g, s = h.grad(p, target)
+        acc += g
+        sacc += s
+    h.set_band(0, 0)
+    lg = O.loss_grad(opar(pool), target.cpu().numpy().astype(np.float64))
+    assert_grads(acc.cpu().numpy(), lg.grad, lg.grad_abs, what="band sum")
+    assert abs(float(sacc[0]) - float(fs[0])) < 1e-9 * float(fs[0])
+
+
+# --------------------------------------------------------------- Adam a8 ----
+
+@pytest.mark.parametrize("C,order", [(1, 0), (3, 1)])
+def test_step_matches_oracle_adam(C, order):
+    H, W, K = 40, 44, 30
+    pool = conditioned(synth.aniso_pool(H, W, C, K, 50 + C, order=order, log_pi_sd=0.3), H, W)
+    target = synth.image(H, W, C, 51)
+    h = smoe.SMoE(K, H, W, C, order)
+    p = dev_pool(pool)
+    lr = smoe.LR(mu=0.01, chol=1e-3, log_pi=1e-3, expert=1e-3, slope=2e-4)
+    st = h.step(p, torch.as_tensor(target).cuda(), lr)
+    op = opar(pool)
+    lg = O.loss_grad(op, target.astype(np.float64))
+    assert abs(st.loss - lg.loss) <= 1e-5 * lg.loss
+    assert abs(st.psnr_db - lg.psnr) < 1e-4
+    opt = O.Adam(K, op.Pk)
+    ref = opt.step(op, lg.grad, O.LR(0.01, 1e-3, 1e-3, 1e-3, 2e-4)).flat()
+    got = p.flat().cpu().numpy().astype(np.float64)
+    lrv = O.LR(0.01, 1e-3, 1e-3, 1e-3, 2e-4).vector(C, order)
+    # first Adam step moves each parameter by lr * g / (|g| + eps): compare
+    # the update within 1e-3 of its learning rate (plus fp32 rounding of p)
+    tol = 1e-3 * lrv[None, :] + 2e-7 * np.abs(ref)
+    small = np.abs(lg.grad) < 1e-5 * lg.grad_abs + 1e-7          # sign not determined
+    bad = (np.abs(got - ref) > tol) & ~small
+    assert not bad.any(), np.argwhere(bad)[:5]
+
+
+def test_clamp_and_nonfinite():
+    H, W, K = 24, 24, 4
+    pool = synth.aniso_pool(H, W, 1, K, 3)
+    pool.chol[:, 0] = 1.2e-3
+    pool.chol[:, 2] = 1.1e-3
+    h = smoe.SMoE(K, H, W, 1, 0)
+    p = dev_pool(pool)
+    target = torch.rand((1, H, W), device="cuda")
+    h.step(p, target, smoe.LR(mu=0, chol=0.5, expert=0))
+    c = p.chol.cpu().numpy()
+    assert (c[:, 0] >= 1e-3).all() and (c[:, 2] >= 1e-3).all()
+    p.mu[0, 0] = float("nan")
+    with pytest.raises(smoe.SmoeError) as e:
+        h.step(p, target, smoe.LR())
+    assert e.value.status == smoe.ERR_NONFINITE
+
+
+def test_capacity_overflow_is_recovered():
+    H, W, K = 256, 256, 400
+    pool = conditioned(synth.aniso_pool(H, W, 1, K, 12), H, W)
+    target = torch.as_tensor(synth.image(H, W, 1, 13)).cuda()
+    h = smoe.SMoE(K, H, W, 1, 0)
+    p = dev_pool(pool)
+    st_small = h.step(p, target, smoe.LR())      # calibrates the capacity
+    big = p.clone()
+    big.chol *= 8.0                              # ~64x more pairs
+    ref = big.clone()
+    st = h.step(big, target, smoe.LR())          # synchronous: grows and redoes
+    assert st.pairs > 4 * (st_small.pairs * 1.25 + 4096)
+    h2 = smoe.SMoE(K, H, W, 1, 0)
+    st2 = h2.step(ref, target, smoe.LR())
+    assert st.pairs == st2.pairs and abs(st.loss - st2.loss) < 1e-6 * st2.loss
+    # asynchronous path: the overflowing call is skipped and reported
+    h3 = smoe.SMoE(K, H, W, 1, 0)
+    q = p.clone()
+    h3.step(q, target, smoe.LR())
+    q2 = q.clone()
+    q2.chol *= 8.0
+    before = q2.flat().clone()
+    h3.step(q2, target, smoe.LR(), stats=False)
+    with pytest.raises(smoe.SmoeError) as e:
+        h3.sync()
+    assert e.value.status == smoe.ERR_CAPACITY
+    assert torch.equal(q2.flat(), before)        # skipped: parameters untouched
+    h3.step(q2, target, smoe.LR(), stats=False)
+    h3.sync()
+    assert not torch.equal(q2.flat(), before)
+
+
+# ----------------------------------------------------------- 100-iter fit ---
+
+@pytest.mark.parametrize("init", ["paper", "aniso"])
+def test_fit_100_iterations(init):
+    """Config 1 geometry (64x64 gray, 64 kernels, constant experts): PSNR
+    after 100 Adam iterations within 0.01 dB of the oracle, parameters within
+    1e-3 relative (floor: lr x iterations x 1e-3)."""
+    H, W, C, K, T = 64, 64, 1, 64, 100
+    target = synth.image(H, W, C, 1235)
+    if init == "paper":
+        pool = synth.paper_init(target, K, 1236)
+    else:
+        pool = synth.aniso_pool(H, W, C, K, 1237, l_range=(3, 8), shear=3)
+    pool = conditioned(pool, H, W)
+    h = smoe.SMoE(K, H, W, C, 0)
+    p = dev_pool(pool)
+    tg = torch.as_tensor(target).cuda()
+    trace = []
+    for t in range(T):
+        st = h.step(p, tg, smoe.LR.paper(t, T))
+        trace.append(st.psnr_db)
+    q, otrace = O.fit(opar(pool), target.astype(np.float64), T)
+    final = O.loss_grad(q, target.astype(np.float64)).psnr
+    fin_gpu = h.grad(p, tg)[1][1].item()
+    psnr_gpu = 10 * np.log10(H * W * C / fin_gpu)
+    assert abs(psnr_gpu - final) < 0.01, (psnr_gpu, final)
+    assert abs(trace[-1] - otrace[-1][1]) < 0.01
+    got = p.flat().cpu().numpy().astype(np.float64)
+    ref = q.flat()
+    lrv = O.LR().vector(C, 0)
+    tol = 1e-3 * np.abs(ref - opar(pool).flat()) + 1e-3 * lrv[None, :] * 10
+    assert (np.abs(got - ref) <= tol + 1e-5 * np.abs(ref)).mean() > 0.99
+
+
+# --------------------------------------------------- full-size sampled ------
+
+def test_kodak_full_size_sampled_parity():
+    """Config 2 at full size (768x512x3, 10k kernels, linear experts) in the
+    launch configuration bench.py times: 2000 sampled pixels and 16 sampled
+    kernels' gradients against the dense oracle."""
+    target, _, pool = synth.workload("kodak")
+    H, W = target.shape[1:]
+    g = np.random.default_rng(5)
+    pool.expert[:, :, 1:] = g.normal(0, 0.01, pool.expert[:, :, 1:].shape).astype(np.float32)
+    pool = conditioned(pool, H, W)
+    K = pool.K
+    h = smoe.SMoE(K, H, W, 3, 1)
+    p = dev_pool(pool)
+    y = h.render(p).cpu().numpy()
+    ix = g.integers(0, W, 2000)
+    iy = g.integers(0, H, 2000)
+    op = opar(pool)
+    y_ref, _ = O.render_points(op, ix.astype(float), iy.astype(float))
+    assert_pixels(y[:, iy, ix].T, y_ref)
+    grad, _ = h.grad(p, torch.as_tensor(target).cuda())
+    sel = g.choice(K, 16, replace=False)
+    g_ref, a_ref = O.grad_kernels(op, target.astype(np.float64), sel)
+    assert_grads(grad.cpu().numpy()[sel], g_ref, a_ref)
