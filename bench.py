@@ -163,6 +163,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--backward-mode", type=int, default=0, help="0 kernel-parallel, 1 pixel-parallel")
     args = ap.parse_args()
     assert args.warmup >= 3, "at least 3 warm-up steps"
     if args.impl == "reference":
@@ -184,7 +185,7 @@ def main():
     dev = torch.device("cuda", local)
     tgt = torch.as_tensor(target).to(dev)
     params = smoe.Params.from_numpy(pool, dev)
-    h = smoe.SMoE(K, H, W, C, order, device=local)
+    h = smoe.SMoE(K, H, W, C, order, device=local, backward_mode=args.backward_mode)
     fit = BandedFit(h, rank, world) if world > 1 else None
     T_total = args.warmup + args.steps
 

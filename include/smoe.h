@@ -97,6 +97,9 @@ typedef struct {
     double R2;                     /* truncation radius^2; default 2 ln 100 (Q1) */
     int device;                    /* CUDA device ordinal, -1 = current device   */
     long long pair_capacity;       /* initial pair capacity, 0 = automatic        */
+    int backward_mode;             /* 0 = kernel-parallel over ellipse masks
+                                      (default), 1 = pixel-parallel with warp
+                                      reductions                 */
 } smoe_options;
 
 /* Fill `o` with the defaults (R2 = 2 ln 100, device = -1, automatic capacity). */
@@ -176,14 +179,12 @@ smoe_lr smoe_paper_lr(int t, int T);
  * roofline).  smoe_profile_end: synchronise, return per-kernel
  * totals in times[SMOE_KERNEL_COUNT] and the work counters, stop profiling. */
 enum {
-    SMOE_KERNEL_PREPROCESS = 0,
-    SMOE_KERNEL_SCAN = 1,
-    SMOE_KERNEL_SCATTER = 2,
-    SMOE_KERNEL_SORT = 3,
-    SMOE_KERNEL_RASTER_TRAIN = 4,
-    SMOE_KERNEL_RASTER_RENDER = 5,
-    SMOE_KERNEL_ADAM = 6,
-    SMOE_KERNEL_COUNT = 7
+    SMOE_KERNEL_PREPROCESS = 0,    /* a1 + a2 (the last CTA scans)          */
+    SMOE_KERNEL_SCATTER = 1,       /* a3                                     */
+    SMOE_KERNEL_RASTER_TRAIN = 2,  /* a4 (bucket sort) + a5-a7               */
+    SMOE_KERNEL_RASTER_RENDER = 3, /* a4 + a5/a9                             */
+    SMOE_KERNEL_ADAM = 4,          /* a8                                     */
+    SMOE_KERNEL_COUNT = 5
 };
 typedef struct {
     double total_ms;

@@ -79,6 +79,7 @@ struct smoe_ctx {
     int band0 = 0, band1 = 0;   // tile rows; band1 == 0 -> whole image
     long long launches = 0;
     long long init_cap = 0;
+    int bwd_mode = 0;
     Prof prof;
     std::string err;
 };
@@ -229,16 +230,13 @@ void check_params(const smoe_params *p)
 void bin(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_hi, bool zero_stats)
 {
     int K = h->K;
-    int nb = (K + 255) / 256;
+    int nb = (K + PRE_NT - 1) / PRE_NT;
     float sx = (float)g.oW / (float)h->W, sy = (float)g.oH / (float)h->H;
     launch(h, SMOE_KERNEL_PREPROCESS, "k_preprocess", [&] {
-        DISPATCH_CE(h, (k_preprocess<C_, E_><<<nb, 256, 0, h->stream>>>(
+        DISPATCH_CE(h, (k_preprocess<C_, E_><<<nb, PRE_NT, 0, h->stream>>>(
                            K, pdev(p), h->R2, sx, sy, g.oW, g.oH, g.nx, ty_lo, ty_hi, h->rec, h->tbox,
-                           g.cnt, &h->ctl->hc)));
-    });
-    launch(h, SMOE_KERNEL_SCAN, "k_scan", [&] {
-        k_scan<<<1, 1024, 0, h->stream>>>(g.cnt, g.n_tiles, g.start, g.cursor, g.cap, g.gc,
-                                          zero_stats ? h->ctl->dstats : nullptr);
+                           g.cnt, &h->ctl->hc, g.n_tiles, g.start, g.cursor, g.cap, g.gc,
+                           zero_stats ? h->ctl->dstats : nullptr)));
     });
     if (!g.calibrated) {
         long long P;
@@ -246,15 +244,10 @@ void bin(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_hi, bool 
         CK(cudaStreamSynchronize(h->stream));
         grow(h, g, P > h->init_cap ? P : h->init_cap);
     }
+    int ns = (K + 63) / 64;
     launch(h, SMOE_KERNEL_SCATTER, "k_scatter", [&] {
-        k_scatter<<<nb, 256, 0, h->stream>>>(K, h->tbox, g.nx, ty_lo, ty_hi, g.cursor, g.ids, g.cap, g.gc);
+        k_scatter<<<ns, 64, 0, h->stream>>>(K, h->tbox, g.nx, ty_lo, ty_hi, g.cursor, g.ids, g.cap, g.gc);
     });
-    int nt = (ty_hi - ty_lo) * g.nx;
-    if (nt > 0) {
-        launch(h, SMOE_KERNEL_SORT, "k_sort_segs", [&] {
-            k_sort_segs<<<nt, 256, 0, h->stream>>>(g.start, g.ids, g.tmp, ty_lo * g.nx, g.cap, g.gc);
-        });
-    }
 }
 
 void band_rows(smoe_ctx *h, int &ty_lo, int &ty_hi)
@@ -285,7 +278,7 @@ void forward_backward(smoe_ctx *h, const smoe_params *p, const float *target)
     int nt = (ty_hi - ty_lo) * g.nx;
     if (nt <= 0) return;
     RasterArgs A{};
-    A.rec = h->rec; A.ids = g.ids; A.start = g.start; A.gc = g.gc; A.cap = g.cap;
+    A.rec = h->rec; A.ids = g.ids; A.tmp = g.tmp; A.start = g.start; A.gc = g.gc; A.cap = g.cap;
     A.nx = g.nx; A.tile0 = ty_lo * g.nx; A.oW = h->W; A.oH = h->H;
     A.sx = 1.0f; A.sy = 1.0f; A.R2 = h->R2;
     A.target = target;
@@ -293,8 +286,11 @@ void forward_backward(smoe_ctx *h, const smoe_params *p, const float *target)
     A.acc = h->acc; A.dstats = h->ctl->dstats; A.out = nullptr;
     A.work = h->prof.d_work;
     launch(h, SMOE_KERNEL_RASTER_TRAIN, "k_raster<train>", [&] {
-        if (h->prof.on) DISPATCH_CE(h, (k_raster<C_, E_, true, true><<<nt, 128, 0, h->stream>>>(A)));
-        else DISPATCH_CE(h, (k_raster<C_, E_, true, false><<<nt, 128, 0, h->stream>>>(A)));
+        bool kp = h->bwd_mode == 0;
+        if (h->prof.on && kp) DISPATCH_CE(h, (k_raster<C_, E_, true, true, true><<<nt, 128, 0, h->stream>>>(A)));
+        else if (kp) DISPATCH_CE(h, (k_raster<C_, E_, true, false, true><<<nt, 128, 0, h->stream>>>(A)));
+        else if (h->prof.on) DISPATCH_CE(h, (k_raster<C_, E_, true, true, false><<<nt, 128, 0, h->stream>>>(A)));
+        else DISPATCH_CE(h, (k_raster<C_, E_, true, false, false><<<nt, 128, 0, h->stream>>>(A)));
     });
 }
 
@@ -302,7 +298,7 @@ void launch_adam(smoe_ctx *h, int mode, const smoe_params *p, const float *grad_
                  const smoe_lr *lr)
 {
     int K = h->K;
-    int nb = (K + 255) / 256;
+    int nb = (K + 63) / 64;
     ParamsMut pm{p->mu, p->chol, p->log_pi, p->expert};
     LrDev l{0, 0, 0, 0, 0};
     if (lr) l = LrDev{lr->mu, lr->chol, lr->log_pi, lr->expert, lr->slope};
@@ -310,13 +306,13 @@ void launch_adam(smoe_ctx *h, int mode, const smoe_params *p, const float *grad_
     long long cap = h->train.cap;
     launch(h, SMOE_KERNEL_ADAM, "k_adam", [&] {
         if (mode == 0)
-            DISPATCH_CE(h, (k_adam<C_, E_, 0><<<nb, 256, 0, h->stream>>>(K, pm, h->acc, nullptr, nullptr, h->m1,
+            DISPATCH_CE(h, (k_adam<C_, E_, 0><<<nb, 64, 0, h->stream>>>(K, pm, h->acc, nullptr, nullptr, h->m1,
                                                                            h->m2, l, &h->ctl->hc, gc, cap)));
         else if (mode == 1)
-            DISPATCH_CE(h, (k_adam<C_, E_, 1><<<nb, 256, 0, h->stream>>>(K, pm, h->acc, nullptr, grad_out, h->m1,
+            DISPATCH_CE(h, (k_adam<C_, E_, 1><<<nb, 64, 0, h->stream>>>(K, pm, h->acc, nullptr, grad_out, h->m1,
                                                                            h->m2, l, &h->ctl->hc, gc, cap)));
         else
-            DISPATCH_CE(h, (k_adam<C_, E_, 2><<<nb, 256, 0, h->stream>>>(K, pm, h->acc, grad_in, nullptr, h->m1,
+            DISPATCH_CE(h, (k_adam<C_, E_, 2><<<nb, 64, 0, h->stream>>>(K, pm, h->acc, grad_in, nullptr, h->m1,
                                                                            h->m2, l, &h->ctl->hc, gc, cap)));
     });
 }
@@ -410,7 +406,8 @@ smoe_status smoe_create_ex(const smoe_options *o, smoe_handle *out)
     if (!o || !out) { g_err = "NULL argument"; return SMOE_ERR_INVALID_ARG; }
     *out = nullptr;
     if (o->K < 1 || o->H < 1 || o->W < 1 || !(o->C == 1 || o->C == 3) ||
-        !(o->expert_order == 0 || o->expert_order == 1) || !(o->R2 > 0)) {
+        !(o->expert_order == 0 || o->expert_order == 1) || !(o->R2 > 0) ||
+        !(o->backward_mode == 0 || o->backward_mode == 1)) {
         g_err = "smoe_create: need K,H,W >= 1, C in {1,3}, expert_order in {0,1}, R2 > 0";
         return SMOE_ERR_INVALID_ARG;
     }
@@ -427,6 +424,7 @@ smoe_status smoe_create_ex(const smoe_options *o, smoe_handle *out)
     h->V = h->P <= 8 ? 8 : 16;
     h->R2 = (float)o->R2;
     h->init_cap = o->pair_capacity;
+    h->bwd_mode = o->backward_mode;
     int dev = o->device;
     if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) {
         (void)cudaGetLastError();
@@ -618,14 +616,14 @@ smoe_status smoe_render(smoe_handle h, const smoe_params *p, int out_H, int out_
             size_t n = (size_t)h->C * out_H * out_W;
             float *o = odev ? out : stage(h->stage_out, h->stage_out_n, n);
             RasterArgs A{};
-            A.rec = h->rec; A.ids = g.ids; A.start = g.start; A.gc = g.gc; A.cap = g.cap;
+            A.rec = h->rec; A.ids = g.ids; A.tmp = g.tmp; A.start = g.start; A.gc = g.gc; A.cap = g.cap;
             A.nx = g.nx; A.tile0 = 0; A.oW = out_W; A.oH = out_H;
             A.sx = (float)h->W / (float)out_W; A.sy = (float)h->H / (float)out_H;
             A.R2 = h->R2; A.out = o;
             A.work = h->prof.d_work;
             launch(h, SMOE_KERNEL_RASTER_RENDER, "k_raster<render>", [&] {
-                if (h->prof.on) DISPATCH_CE(h, (k_raster<C_, E_, false, true><<<g.n_tiles, 128, 0, h->stream>>>(A)));
-                else DISPATCH_CE(h, (k_raster<C_, E_, false, false><<<g.n_tiles, 128, 0, h->stream>>>(A)));
+                if (h->prof.on) DISPATCH_CE(h, (k_raster<C_, E_, false, true, false><<<g.n_tiles, 128, 0, h->stream>>>(A)));
+                else DISPATCH_CE(h, (k_raster<C_, E_, false, false, false><<<g.n_tiles, 128, 0, h->stream>>>(A)));
             });
             if (odev) return SMOE_OK;
             read_ctl(h);
@@ -642,28 +640,34 @@ smoe_status smoe_bin(smoe_handle h, const smoe_params *p, int out_H, int out_W, 
                      long long ids_cap, long long *n_pairs, int *tilebox)
 {
     if (!h) return SMOE_ERR_BAD_HANDLE;
-    return guard(h, [&]() -> smoe_status {
-        check_params(p);
-        if (out_H < 1 || out_W < 1) throw SmoeError(SMOE_ERR_INVALID_ARG, "smoe_bin: bad raster");
-        for (int attempt = 0;; attempt++) {
-            Grid &g = h->render;
-            ensure_grid(h, g, &h->ctl->render, out_H, out_W);
-            bin(h, g, p, 0, g.ny, false);
+    if (out_H < 1 || out_W < 1) { set_err(h, "smoe_bin: bad raster"); return SMOE_ERR_INVALID_ARG; }
+    // The lists are reported exactly as the hot path leaves them: a render
+    // on the out_H x out_W raster bins (a1-a3) and its raster CTAs sort their
+    // buckets in place (a4).
+    smoe_status st = guard(h, [&]() -> smoe_status {
+        size_t n = (size_t)h->C * out_H * out_W;
+        float *scratch = nullptr;
+        CK(cudaMalloc(&scratch, n * sizeof(float)));
+        smoe_status s2 = smoe_render(h, p, out_H, out_W, scratch);
+        if (s2 == SMOE_OK) {
             read_ctl(h);
-            smoe_status st = faults(h);
-            if (st == SMOE_ERR_CAPACITY && attempt < 3) continue;
-            if (st != SMOE_OK) return st;
-            long long P = h->h_ctl->render.pairs;
-            if (n_pairs) *n_pairs = P;
-            if (tile_range)
-                CK(cudaMemcpy(tile_range, g.start, sizeof(int) * (g.n_tiles + 1), cudaMemcpyDefault));
-            if (ids) {
-                if (ids_cap < P) throw SmoeError(SMOE_ERR_INVALID_ARG, "smoe_bin: ids_cap < P");
-                CK(cudaMemcpy(ids, g.ids, sizeof(int) * P, cudaMemcpyDefault));
-            }
-            if (tilebox) CK(cudaMemcpy(tilebox, h->tbox, sizeof(int4) * h->K, cudaMemcpyDefault));
-            return SMOE_OK;
+            s2 = faults(h);
         }
+        cudaFree(scratch);
+        return s2;
+    });
+    if (st != SMOE_OK) return st;
+    return guard(h, [&]() -> smoe_status {
+        Grid &g = h->render;
+        long long P = h->h_ctl->render.pairs;
+        if (n_pairs) *n_pairs = P;
+        if (tile_range) CK(cudaMemcpy(tile_range, g.start, sizeof(int) * (g.n_tiles + 1), cudaMemcpyDefault));
+        if (ids) {
+            if (ids_cap < P) throw SmoeError(SMOE_ERR_INVALID_ARG, "smoe_bin: ids_cap < P");
+            CK(cudaMemcpy(ids, g.ids, sizeof(int) * P, cudaMemcpyDefault));
+        }
+        if (tilebox) CK(cudaMemcpy(tilebox, h->tbox, sizeof(int4) * h->K, cudaMemcpyDefault));
+        return SMOE_OK;
     });
 }
 
@@ -671,8 +675,8 @@ long long smoe_launch_count(smoe_handle h) { return h ? h->launches : -1; }
 
 const char *smoe_kernel_name(int id)
 {
-    static const char *names[SMOE_KERNEL_COUNT] = {"k_preprocess", "k_scan", "k_scatter", "k_sort_segs",
-                                                   "k_raster<train>", "k_raster<render>", "k_adam"};
+    static const char *names[SMOE_KERNEL_COUNT] = {"k_preprocess", "k_scatter", "k_raster<train>",
+                                                   "k_raster<render>", "k_adam"};
     return (id >= 0 && id < SMOE_KERNEL_COUNT) ? names[id] : "?";
 }
 

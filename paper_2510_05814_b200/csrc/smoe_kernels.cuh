@@ -4,11 +4,11 @@
 // Q-numbers = readings in DESIGN.md.  Pipeline of one step:
 //
 //   k_preprocess  per kernel: whitening record, square 99% box,
-//                 per-block overlap counts (atomics)             [§8(a) a1]
-//   k_scan        exclusive scan of block counts -> block ranges  [a2/a4]
+//                 per-block overlap counts (atomics); the last CTA
+//                 scans the counts into block ranges               [§8(a) a1, a2]
 //   k_scatter     kernel ids into their blocks' buckets           [a3]
-//   k_sort_segs   in-bucket sort by kernel id (second radix digit)[a4]
-//   k_raster      per 16x16 block: forward, loss, backward         [a5-a7, a9]
+//   k_raster      per 16x16 block: bucket sort by kernel id (second
+//                 radix digit), forward, loss, backward            [a4-a7, a9]
 //   k_adam        chain rule -> Adam -> clamp, accumulator reset   [a8]
 //
 // The binning is an MSD radix sort of the key (tile_id | kernel_id): the
@@ -33,6 +33,8 @@ struct GridCtr {
     long long pairs;      // P of the most recent binning on this grid
     long long need;       // latched: largest P that exceeded the capacity
     long long skipped;    // latched: sequences skipped because of overflow
+    unsigned int ticket;  // last-CTA ticket of k_preprocess
+    unsigned int pad;
 };
 
 // Per-handle device counters.
@@ -71,6 +73,75 @@ __device__ __forceinline__ float ex2_approx(float x)
 
 __device__ __forceinline__ bool finitef(float x) { return isfinite(x); }
 
+// ------------------------------------------------------------ a2 / a4 -----
+// Exclusive scan of the per-block counts by one CTA of NT threads (4 counts
+// per thread per round).  Produces start[n+1] and the scatter cursors, zeroes
+// the counts for the next binning, publishes P and latches overflow; also
+// zeroes the loss partials consumed by the raster that follows.  Run by the
+// last CTA of k_preprocess to finish (all count atomics are visible then).
+template <int NT>
+__device__ __forceinline__ void scan_counts(int *__restrict__ cnt, int n, int *__restrict__ start,
+                                            int *__restrict__ cursor, long long cap, GridCtr *gc,
+                                            double *dstats)
+{
+    constexpr int NW = NT / 32;
+    __shared__ int warp_tot[NW];
+    __shared__ long long carry_s;
+    int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) carry_s = 0;
+    if (tid < 4 && dstats) dstats[tid] = 0.0;
+    __syncthreads();
+    for (int base = 0; base < n; base += 4 * NT) {
+        int i0 = base + tid * 4;
+        int v[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) v[q] = (i0 + q < n) ? __ldcg(cnt + i0 + q) : 0;
+        int loc = v[0] + v[1] + v[2] + v[3];
+        int incl = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) warp_tot[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            int w = lane < NW ? warp_tot[lane] : 0;
+            int wi = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int t = __shfl_up_sync(FULL, wi, o);
+                if (lane >= o) wi += t;
+            }
+            if (lane < NW) warp_tot[lane] = wi - w;  // exclusive
+        }
+        __syncthreads();
+        long long carry = carry_s;
+        int ex = (int)carry + warp_tot[wid] + incl - loc;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            if (i0 + q < n) {
+                start[i0 + q] = ex;
+                cursor[i0 + q] = ex;
+                cnt[i0 + q] = 0;
+            }
+            ex += v[q];
+        }
+        __syncthreads();
+        if (tid == NT - 1) carry_s = carry + warp_tot[NW - 1] + incl;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        long long P = carry_s;
+        start[n] = (int)P;
+        gc->pairs = P;
+        if (P > cap) {
+            if (P > gc->need) gc->need = P;
+            gc->skipped += 1;
+        }
+    }
+}
+
 // ---------------------------------------------------------------- a1 ------
 // Geometry shader: Sigma = L L^T, lambda_max in closed form,
 // square box of half side r = sqrt(R2 lambda_max), pixel-centre rule (Q5)
@@ -79,14 +150,12 @@ __device__ __forceinline__ bool finitef(float x) { return isfinite(x); }
 // Whitening: u = a dx, v = b dx + c dy with a = 1/l11, b = -l21/(l11 l22),
 // c = 1/l22, so d^2 = u^2 + v^2 = delta^T Sigma^-1 delta.
 template <int C, int E>
-__global__ void __launch_bounds__(256)
-k_preprocess(int K, ParamsDev p, float R2, float sx /* oW/W */, float sy /* oH/H */, int oW, int oH,
-             int nx, int ty_lo, int ty_hi, float *__restrict__ rec,
-             int4 *__restrict__ tbox, int *__restrict__ cnt, HandleCtr *hc)
+__device__ __forceinline__ void
+preprocess_one(int k, ParamsDev p, float R2, float sx, float sy, int oW, int oH,
+               int nx, int ty_lo, int ty_hi, float *__restrict__ rec,
+               int4 *__restrict__ tbox, int *__restrict__ cnt, HandleCtr *hc)
 {
     using R = Rec<C, E>;
-    int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= K) return;
     float2 mu = reinterpret_cast<const float2 *>(p.mu)[k];
     float l11 = p.chol[3 * k], l21 = p.chol[3 * k + 1], l22 = p.chol[3 * k + 2];
     float lp = p.log_pi[k];
@@ -127,76 +196,37 @@ k_preprocess(int K, ParamsDev p, float R2, float sx /* oW/W */, float sy /* oH/H
     tbox[k] = tb;
 }
 
-// ------------------------------------------------------------ a2 / a4 -----
-// Exclusive scan of the per-block counts (one CTA of 1024 threads, 4096
-// counts per round).  Produces start[n+1] and the scatter cursors, zeroes the
-// counts for the next binning, publishes P and latches overflow.  Also zeroes
-// the loss partials consumed by the raster that follows.
-__global__ void __launch_bounds__(1024)
-k_scan(int *__restrict__ cnt, int n, int *__restrict__ start, int *__restrict__ cursor,
-       long long cap, GridCtr *gc, double *dstats)
+constexpr int PRE_NT = 256;
+
+template <int C, int E>
+__global__ void __launch_bounds__(PRE_NT)
+k_preprocess(int K, ParamsDev p, float R2, float sx /* oW/W */, float sy /* oH/H */, int oW, int oH,
+             int nx, int ty_lo, int ty_hi, float *__restrict__ rec,
+             int4 *__restrict__ tbox, int *__restrict__ cnt, HandleCtr *hc,
+             int n_tiles, int *__restrict__ start, int *__restrict__ cursor, long long cap,
+             GridCtr *gc, double *dstats)
 {
-    __shared__ int warp_tot[32];
-    __shared__ long long carry_s;
-    int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    if (tid == 0) carry_s = 0;
-    if (tid < 4 && dstats) dstats[tid] = 0.0;
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < K) preprocess_one<C, E>(k, p, R2, sx, sy, oW, oH, nx, ty_lo, ty_hi, rec, tbox, cnt, hc);
+    // the last CTA to finish scans the counts (a2)
+    __shared__ bool last;
     __syncthreads();
-    for (int base = 0; base < n; base += 4096) {
-        int i0 = base + tid * 4;
-        int v[4];
-#pragma unroll
-        for (int q = 0; q < 4; q++) v[q] = (i0 + q < n) ? cnt[i0 + q] : 0;
-        int loc = v[0] + v[1] + v[2] + v[3];
-        int incl = loc;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int t = __shfl_up_sync(FULL, incl, o);
-            if (lane >= o) incl += t;
-        }
-        if (lane == 31) warp_tot[wid] = incl;
-        __syncthreads();
-        if (wid == 0) {
-            int w = warp_tot[lane];
-            int wi = w;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                int t = __shfl_up_sync(FULL, wi, o);
-                if (lane >= o) wi += t;
-            }
-            warp_tot[lane] = wi - w;  // exclusive
-        }
-        __syncthreads();
-        long long carry = carry_s;
-        int ex = (int)carry + warp_tot[wid] + incl - loc;
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-            if (i0 + q < n) {
-                start[i0 + q] = ex;
-                cursor[i0 + q] = ex;
-                cnt[i0 + q] = 0;
-            }
-            ex += v[q];
-        }
-        __syncthreads();
-        if (tid == 1023) carry_s = carry + warp_tot[31] + incl;
-        __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&gc->ticket, 1u) == gridDim.x - 1;
     }
-    if (tid == 0) {
-        long long P = carry_s;
-        start[n] = (int)P;
-        gc->pairs = P;
-        if (P > cap) {
-            if (P > gc->need) gc->need = P;
-            gc->skipped += 1;
-        }
-    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    scan_counts<PRE_NT>(cnt, n_tiles, start, cursor, cap, gc, dstats);
+    if (threadIdx.x == 0) gc->ticket = 0;
 }
+
 
 // ---------------------------------------------------------------- a3 ------
 // First radix digit: every block b_n inside kernel k's box records k
 // ("Each intersected block b_n is recorded").
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(64)
 k_scatter(int K, const int4 *__restrict__ tbox, int nx, int ty_lo, int ty_hi,
           int *__restrict__ cursor, int *__restrict__ ids, long long cap, const GridCtr *gc)
 {
@@ -206,11 +236,24 @@ k_scatter(int K, const int4 *__restrict__ tbox, int nx, int ty_lo, int ty_hi,
     int4 tb = tbox[k];
     if (tb.x < 0) return;
     int y0 = max(tb.z, ty_lo), y1 = min(tb.w, ty_hi - 1);
-    for (int ty = y0; ty <= y1; ty++)
-        for (int tx = tb.x; tx <= tb.y; tx++) {
-            int pos = atomicAdd(&cursor[ty * nx + tx], 1);
-            ids[pos] = k;
+    if (y0 > y1) return;
+    const int w = tb.y - tb.x + 1, cnt = w * (y1 - y0 + 1);
+    // issue the bucket atomics in groups of 8 so their latencies overlap
+    for (int i0 = 0; i0 < cnt; i0 += 8) {
+        int pos[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            int i = i0 + q;
+            pos[q] = -1;
+            if (i < cnt) {
+                int tyy = y0 + i / w, txx = tb.x + i % w;
+                pos[q] = atomicAdd(&cursor[tyy * nx + txx], 1);
+            }
         }
+#pragma unroll
+        for (int q = 0; q < 8; q++)
+            if (pos[q] >= 0) ids[pos[q]] = k;
+    }
 }
 
 // ---------------------------------------------------------------- a4 ------
@@ -244,29 +287,74 @@ __device__ __forceinline__ int lower_bound_i(const int *a, int n, int x)
     return lo;
 }
 
-__global__ void __launch_bounds__(256)
-k_sort_segs(const int *__restrict__ start, int *__restrict__ ids, int *__restrict__ tmp,
-            int tile0, long long cap, const GridCtr *gc)
+// Warp-level bitonic sort of up to 32*R ints held in registers, element
+// e = i*32 + lane (coalesced loads/stores).  Stages with partner distance
+// j < 32 exchange through shuffles, j >= 32 swap registers of one lane.
+template <int R>
+__device__ __forceinline__ void warp_bitonic(int (&v)[R], int lane)
 {
-    __shared__ int s[SORT_CAP];
-    if (gc->pairs > cap) return;
-    int t = tile0 + blockIdx.x;
-    int b = start[t], n = start[t + 1] - b;
-    if (n <= 1) return;
-    int *seg = ids + b;
-    for (int c0 = 0; c0 < n; c0 += SORT_CAP) {
-        int m = min(SORT_CAP, n - c0);
+#pragma unroll
+    for (int k = 2; k <= 32 * R; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j < 32) {
+#pragma unroll
+                for (int i = 0; i < R; i++) {
+                    int e = i * 32 + lane;
+                    int o = __shfl_xor_sync(FULL, v[i], j);
+                    bool asc = (e & k) == 0, lower = (lane & j) == 0;
+                    v[i] = (lower == asc) ? min(v[i], o) : max(v[i], o);
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < R; i++) {
+                    int ii = i ^ (j >> 5);
+                    if (ii > i) {
+                        int e = i * 32 + lane;
+                        bool asc = (e & k) == 0;
+                        int a = v[i], b = v[ii];
+                        v[i] = asc ? min(a, b) : max(a, b);
+                        v[ii] = asc ? max(a, b) : min(a, b);
+                    }
+                }
+            }
+        }
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void warp_sort_seg(int *seg, int n, int lane)
+{
+    int v[R];
+#pragma unroll
+    for (int i = 0; i < R; i++) v[i] = (i * 32 + lane < n) ? seg[i * 32 + lane] : 0x7fffffff;
+    warp_bitonic<R>(v, lane);
+#pragma unroll
+    for (int i = 0; i < R; i++)
+        if (i * 32 + lane < n) seg[i * 32 + lane] = v[i];
+}
+
+// Sort one bucket of n kernel ids in place with the whole CTA: chunks of
+// `chunk` (a power of two fitting the shared buffer s) are bitonic-sorted in
+// shared memory, then merged pairwise through global scratch `tmp` (ids are
+// unique, so an element's merged position is its index plus its rank in the
+// other run).
+__device__ __noinline__ void cta_sort_seg(int *seg, int n, int *tmp, int *s, int chunk)
+{
+    for (int c0 = 0; c0 < n; c0 += chunk) {
+        int m = min(chunk, n - c0);
         int np = 32;
         while (np < m) np <<= 1;
+        __syncthreads();
         for (int i = threadIdx.x; i < np; i += blockDim.x) s[i] = i < m ? seg[c0 + i] : 0x7fffffff;
         __syncthreads();
         smem_bitonic(s, np);
         for (int i = threadIdx.x; i < m; i += blockDim.x) seg[c0 + i] = s[i];
-        __syncthreads();
     }
-    if (n <= SORT_CAP) return;
-    int *src = seg, *dst = tmp + b;
-    for (int run = SORT_CAP; run < n; run <<= 1) {
+    __syncthreads();
+    if (n <= chunk) return;
+    int *src = seg, *dst = tmp;
+    for (int run = chunk; run < n; run <<= 1) {
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             int lo = (i / (2 * run)) * (2 * run);
             int mid = min(lo + run, n), hi = min(lo + 2 * run, n);
@@ -281,12 +369,34 @@ k_sort_segs(const int *__restrict__ start, int *__restrict__ ids, int *__restric
     }
     if (src != seg)
         for (int i = threadIdx.x; i < n; i += blockDim.x) seg[i] = src[i];
+    __syncthreads();
+}
+
+// Second radix digit of the binning, run at the start of every raster CTA
+// on its own bucket: <= 256 ids are sorted by warp 0 in registers, larger
+// buckets by the whole CTA.  The sorted bucket is written back, so the global
+// list is the canonical (block, kernel) order that smoe_bin reports.
+__device__ __forceinline__ void sort_bucket(int *seg, int n, int *tmp, int *s, int chunk)
+{
+    if (n <= 1) return;
+    if (n <= 256) {
+        if (threadIdx.x < 32) {
+            int lane = threadIdx.x;
+            if (n <= 32) warp_sort_seg<1>(seg, n, lane);
+            else if (n <= 64) warp_sort_seg<2>(seg, n, lane);
+            else if (n <= 128) warp_sort_seg<4>(seg, n, lane);
+            else warp_sort_seg<8>(seg, n, lane);
+        }
+        return;   // the caller's next __syncthreads publishes the result
+    }
+    cta_sort_seg(seg, n, tmp, s, chunk);
 }
 
 // ------------------------------------------------------- a5 / a6 / a7 -----
 struct RasterArgs {
     const float *rec;
-    const int *ids;
+    int *ids;             // block lists (bucket-sorted in place by the raster)
+    int *tmp;             // merge scratch for buckets larger than the smem chunk
     const int *start;
     const GridCtr *gc;
     long long cap;
@@ -331,21 +441,39 @@ __device__ __forceinline__ float warp_reduce_transpose(float (&v)[V], int lane, 
 
 // One CTA = one 16x16 block b_n, 128 threads = 4 warps, each warp an 8x8
 // quadrant, each lane a vertical pair of pixels.  The block's kernel list
-// K_n is staged through shared memory in batches; a warp skips a kernel when
-// none of its 64 pixels is inside the kernel's ellipse (warp-uniform branch).
-// TRAIN: forward sums D, N_c -> y -> loss partials -> backward sweep over K_n
-// with the per-pixel y, D kept in registers; per (warp, kernel) the raw
-// gradient sums are reduced across the warp and added with one vector of
-// atomics.  RENDER: forward only, y written to out.
-template <int C, int E, bool TRAIN, bool PROF>
+// K_n is staged through shared memory in batches of BATCH; a warp skips a
+// kernel when none of its 64 pixels is inside the kernel's ellipse
+// (warp-uniform branch).
+//
+// Forward (a5): D = sum g, N_c = sum g m_c(x) per pixel in registers.
+// RENDER: y = N/D written to out.  TRAIN: loss partials (a6), then the
+// backward (a7) in one of two forms:
+//   KPAR = false  pixel-parallel: every warp re-sweeps K_n, per (warp,
+//                 kernel) the raw gradient sums are reduced across the warp
+//                 (transpose butterfly) and added with one atomic per value.
+//   KPAR = true   kernel-parallel: the forward records, per kernel, the
+//                 256-bit mask of block pixels inside its ellipse; per-pixel
+//                 backward seeds go to shared memory; then groups of L lanes
+//                 own one kernel each (heaviest first, so lanes of a warp
+//                 carry similar pixel counts) and walk only its masked pixels,
+//                 accumulating the raw sums in registers -- no per-pixel
+//                 reduction, one vector of atomics per kernel and block.
+// Mask bit layout: word 2w+h (warp w, h = upper/lower pixel of the lane's
+// pair), bit l = lane l: col = (w&1)*8 + (l&7), row = (w>>1)*8 + (l>>3)*2 + h.
+template <int C, int E, bool TRAIN, bool PROF, bool KPAR>
 __global__ void __launch_bounds__(128)
 k_raster(RasterArgs A)
 {
     using R = Rec<C, E>;
     constexpr int RS4 = R::RS / 4;
-    constexpr int BATCH = 64;
+    constexpr int BATCH = 128;
+    constexpr bool MASKS = TRAIN && KPAR;
     __shared__ float4 srec[BATCH * RS4];
     __shared__ int sid[BATCH];
+    __shared__ unsigned smask[MASKS ? BATCH : 1][8];
+    __shared__ float4 spix[MASKS ? 256 : 1];      // eD_0..eD_{C-1}, K  (C <= 3)
+    __shared__ int sorder[MASKS ? 128 : 1];          // per-kernel pair offsets
+    __shared__ int sbucket[MASKS ? 4 : 1];           // per-warp totals
     __shared__ double red[3][4];
     if (A.gc->pairs > A.cap) return;
 
@@ -359,6 +487,10 @@ k_raster(RasterArgs A)
     const float ys0 = (py0 + 0.5f) * A.sy - 0.5f, ys1 = (py1 + 0.5f) * A.sy - 0.5f;
     const float R2 = A.R2;
     const int s0 = A.start[tile], n = A.start[tile + 1] - s0;
+    // a4 (second digit): sort this block's bucket by kernel id; srec doubles
+    // as the shared scratch (its capacity in ints is a power of two >= 1024)
+    constexpr int SCHUNK = (BATCH * RS4 * 4 >= 2048) ? 2048 : 1024;
+    sort_bucket(A.ids + s0, n, A.tmp + s0, reinterpret_cast<int *>(srec), SCHUNK);
 
     float D0 = 0.f, D1 = 0.f, N0[C], N1[C];
 #pragma unroll
@@ -376,6 +508,22 @@ k_raster(RasterArgs A)
         }
         __syncthreads();
     };
+    auto load_rec = [&](int j, float (&r)[R::RS]) {
+#pragma unroll
+        for (int q = 0; q < RS4; q++) {
+            float4 f = srec[j * RS4 + q];
+            r[4 * q] = f.x; r[4 * q + 1] = f.y; r[4 * q + 2] = f.z; r[4 * q + 3] = f.w;
+        }
+    };
+    // d^2 of this lane's two pixels for record r
+    auto dist2 = [&](const float (&r)[R::RS], float &dx, float &dy0, float &dy1, float &u, float &w0,
+                     float &w1, float &q0, float &q1) {
+        dx = xs - r[0]; dy0 = ys0 - r[1]; dy1 = ys1 - r[1];
+        u = r[2] * dx;
+        w0 = fmaf(r[3], dx, r[4] * dy0); w1 = fmaf(r[3], dx, r[4] * dy1);
+        float uu = u * u;
+        q0 = fmaf(w0, w0, uu); q1 = fmaf(w1, w1, uu);
+    };
 
     // ---- forward (Eq. 5 with the per-pixel cull of P:221) ----
     for (int b0 = 0; b0 < n; b0 += BATCH) {
@@ -383,22 +531,17 @@ k_raster(RasterArgs A)
         load_batch(b0, nb);
         for (int j = 0; j < nb; j++) {
             float r[R::RS];
-#pragma unroll
-            for (int q = 0; q < RS4; q++) {
-                float4 f = srec[j * RS4 + q];
-                r[4 * q] = f.x; r[4 * q + 1] = f.y; r[4 * q + 2] = f.z; r[4 * q + 3] = f.w;
-            }
-            float dx = xs - r[0], dy0 = ys0 - r[1], dy1 = ys1 - r[1];
-            float u = r[2] * dx;
-            float w0 = fmaf(r[3], dx, r[4] * dy0), w1 = fmaf(r[3], dx, r[4] * dy1);
-            float uu = u * u;
-            float q0 = fmaf(w0, w0, uu), q1 = fmaf(w1, w1, uu);
+            load_rec(j, r);
+            float dx, dy0, dy1, u, w0, w1, q0, q1;
+            dist2(r, dx, dy0, dy1, u, w0, w1, q0, q1);
             bool h0 = v0 && q0 <= R2, h1 = v1 && q1 <= R2;
+            unsigned b0m = __ballot_sync(FULL, h0), b1m = __ballot_sync(FULL, h1);
             if (PROF) {
                 w_tested += w_valid;
-                w_hit += __popc(__ballot_sync(FULL, h0)) + __popc(__ballot_sync(FULL, h1));
+                w_hit += __popc(b0m) + __popc(b1m);
             }
-            if (!__any_sync(FULL, h0 || h1)) continue;
+            if (MASKS && lane == 0 && n <= BATCH) { smask[j][2 * warp] = b0m; smask[j][2 * warp + 1] = b1m; }
+            if ((b0m | b1m) == 0u) continue;
             float g0 = h0 ? ex2_approx(fmaf(q0, -0.5f * LOG2E, r[5])) : 0.f;
             float g1 = h1 ? ex2_approx(fmaf(q1, -0.5f * LOG2E, r[5])) : 0.f;
             D0 += g0; D1 += g1;
@@ -434,9 +577,11 @@ k_raster(RasterArgs A)
     }
 
     // ---- loss / PSNR partials (Q8) and per-pixel backward seeds ----
+    // eD_c = (dL/dy_c) / D and K = sum_c eD_c y_c, so that for a kernel
+    // inside the ellipse G = sum_c eD_c m_c(x) - K and s = dL/d(d^2) = -g G / 2.
     float eD0[C], eD1[C], K0 = 0.f, K1 = 0.f;
-    double sse = 0.0, ssec = 0.0, unc = 0.0;
     {
+        double sse = 0.0, ssec = 0.0, unc = 0.0;
         size_t plane = (size_t)A.oH * A.oW;
 #pragma unroll
         for (int c = 0; c < C; c++) {
@@ -447,7 +592,7 @@ k_raster(RasterArgs A)
             float rc1 = v1 ? __saturatef(y1[c]) - __saturatef(t1) : 0.f;
             sse += (double)(r0 * r0) + (double)(r1 * r1);
             ssec += (double)(rc0 * rc0) + (double)(rc1 * rc1);
-            eD0[c] = A.e_scale * r0 * iD0;      // dL/dy_c / D  (0 if uncovered)
+            eD0[c] = A.e_scale * r0 * iD0;      // 0 if uncovered
             eD1[c] = A.e_scale * r1 * iD1;
             K0 = fmaf(eD0[c], y0[c], K0);
             K1 = fmaf(eD1[c], y1[c], K1);
@@ -460,70 +605,197 @@ k_raster(RasterArgs A)
             unc += __shfl_xor_sync(FULL, unc, o);
         }
         if (lane == 0) { red[0][warp] = sse; red[1][warp] = ssec; red[2][warp] = unc; }
+        if (MASKS) {
+            int c0 = (warp & 1) * 8 + (lane & 7), r0 = (warp >> 1) * 8 + (lane >> 3) * 2;
+            float a0[4] = {0.f, 0.f, 0.f, K0}, a1[4] = {0.f, 0.f, 0.f, K1};
+#pragma unroll
+            for (int c = 0; c < C; c++) { a0[c] = eD0[c]; a1[c] = eD1[c]; }
+            spix[r0 * 16 + c0] = make_float4(a0[0], a0[1], a0[2], a0[3]);
+            spix[(r0 + 1) * 16 + c0] = make_float4(a1[0], a1[1], a1[2], a1[3]);
+        }
         __syncthreads();
         if (threadIdx.x < 3) {
-            double s = red[threadIdx.x][0] + red[threadIdx.x][1] + red[threadIdx.x][2] + red[threadIdx.x][3];
-            if (s != 0.0) atomicAdd(&A.dstats[threadIdx.x], s);
+            double sm = red[threadIdx.x][0] + red[threadIdx.x][1] + red[threadIdx.x][2] + red[threadIdx.x][3];
+            if (sm != 0.0) atomicAdd(&A.dstats[threadIdx.x], sm);
         }
     }
 
-    // ---- backward (appendix of DESIGN.md: raw sums per kernel) ----
-    // s = dL/d(d^2) = -1/2 g G,  G = sum_c eD_c m_c(x) - sum_c eD_c y_c
-    // raw: Su, Sv, Sux(=sum s u dx), Svx, Svy, Ss, then per channel
-    // sum g eD_c (, sum g eD_c dx, sum g eD_c dy)
+    if (!KPAR) {
+        // ---- pixel-parallel backward (raw sums per kernel) ----
+        for (int b0 = 0; b0 < n; b0 += BATCH) {
+            int nb = min(BATCH, n - b0);
+            if (n > BATCH) load_batch(b0, nb);   // n <= BATCH: batch 0 is still resident
+            for (int j = 0; j < nb; j++) {
+                float r[R::RS];
+                load_rec(j, r);
+                float dx, dy0, dy1, u, w0, w1, q0, q1;
+                dist2(r, dx, dy0, dy1, u, w0, w1, q0, q1);
+                bool h0 = v0 && q0 <= R2 && D0 > 0.f, h1 = v1 && q1 <= R2 && D1 > 0.f;
+                if (!__any_sync(FULL, h0 || h1)) continue;
+                float g0 = h0 ? ex2_approx(fmaf(q0, -0.5f * LOG2E, r[5])) : 0.f;
+                float g1 = h1 ? ex2_approx(fmaf(q1, -0.5f * LOG2E, r[5])) : 0.f;
+                float G0 = -K0, G1 = -K1;
+                float acc[R::V];
+#pragma unroll
+                for (int c = 0; c < C; c++) {
+                    float m0 = r[6 + c * E], m1 = m0;
+                    if (E == 3) {
+                        m0 = fmaf(r[6 + c * E + 1], dx, fmaf(r[6 + c * E + 2], dy0, m0));
+                        m1 = fmaf(r[6 + c * E + 1], dx, fmaf(r[6 + c * E + 2], dy1, m1));
+                    }
+                    G0 = fmaf(eD0[c], m0, G0);
+                    G1 = fmaf(eD1[c], m1, G1);
+                    float ge0 = g0 * eD0[c], ge1 = g1 * eD1[c];
+                    acc[6 + c * E] = ge0 + ge1;
+                    if (E == 3) {
+                        acc[6 + c * E + 1] = (ge0 + ge1) * dx;
+                        acc[6 + c * E + 2] = fmaf(ge0, dy0, ge1 * dy1);
+                    }
+                }
+                float sa = -0.5f * g0 * G0, sb = -0.5f * g1 * G1;
+                float sv = fmaf(sa, w0, sb * w1);
+                acc[0] = (sa + sb) * u;
+                acc[1] = sv;
+                acc[2] = (sa + sb) * u * dx;
+                acc[3] = sv * dx;
+                acc[4] = fmaf(sa * w0, dy0, sb * w1 * dy1);
+                acc[5] = sa + sb;
+#pragma unroll
+                for (int i = R::P; i < R::V; i++) acc[i] = 0.f;
+                int idx;
+                float tot = warp_reduce_transpose<R::V>(acc, lane, idx);
+                constexpr int GROUP = 32 / R::V;   // lanes sharing one value index
+                if ((lane & (GROUP - 1)) == 0 && idx < R::P)
+                    atomicAdd(&A.acc[(size_t)sid[j] * R::V + idx], tot);
+            }
+        }
+        return;
+    }
+
+    // ---- kernel-parallel backward over the recorded ellipse masks ----
+    // The batch's (kernel, masked pixel) pairs, kernel-major, are split into
+    // 128 equal contiguous ranges, one per thread: every lane walks the same
+    // number of pairs (balanced), accumulates the raw sums of the current
+    // kernel in registers and flushes them with vector atomics when its range
+    // crosses into the next kernel and at the end.
+    const float tx0 = (float)(tx * TILE), ty0f = (float)(ty * TILE);
     for (int b0 = 0; b0 < n; b0 += BATCH) {
         int nb = min(BATCH, n - b0);
-        if (n > BATCH) load_batch(b0, nb);   // n <= BATCH: batch 0 is still resident
-        for (int j = 0; j < nb; j++) {
-            float r[R::RS];
-#pragma unroll
-            for (int q = 0; q < RS4; q++) {
-                float4 f = srec[j * RS4 + q];
-                r[4 * q] = f.x; r[4 * q + 1] = f.y; r[4 * q + 2] = f.z; r[4 * q + 3] = f.w;
+        if (n > BATCH) {
+            // masks were not kept: reload the batch and redo the cull test
+            load_batch(b0, nb);
+            for (int j = 0; j < nb; j++) {
+                float r[R::RS];
+                load_rec(j, r);
+                float dx, dy0, dy1, u, w0, w1, q0, q1;
+                dist2(r, dx, dy0, dy1, u, w0, w1, q0, q1);
+                unsigned b0m = __ballot_sync(FULL, v0 && q0 <= R2), b1m = __ballot_sync(FULL, v1 && q1 <= R2);
+                if (lane == 0) { smask[j][2 * warp] = b0m; smask[j][2 * warp + 1] = b1m; }
             }
-            float dx = xs - r[0], dy0 = ys0 - r[1], dy1 = ys1 - r[1];
-            float u = r[2] * dx;
-            float w0 = fmaf(r[3], dx, r[4] * dy0), w1 = fmaf(r[3], dx, r[4] * dy1);
-            float uu = u * u;
-            float q0 = fmaf(w0, w0, uu), q1 = fmaf(w1, w1, uu);
-            bool h0 = v0 && q0 <= R2 && D0 > 0.f, h1 = v1 && q1 <= R2 && D1 > 0.f;
-            if (!__any_sync(FULL, h0 || h1)) continue;
-            float g0 = h0 ? ex2_approx(fmaf(q0, -0.5f * LOG2E, r[5])) : 0.f;
-            float g1 = h1 ? ex2_approx(fmaf(q1, -0.5f * LOG2E, r[5])) : 0.f;
-            float G0 = -K0, G1 = -K1;
+            __syncthreads();
+        }
+        // exclusive scan of the per-kernel masked-pixel counts
+        int cnt = 0;
+        if (threadIdx.x < nb) {
+#pragma unroll
+            for (int w = 0; w < 8; w++) cnt += __popc(smask[threadIdx.x][w]);
+        }
+        int inc = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(FULL, inc, o);
+            if (lane >= o) inc += t;
+        }
+        if (lane == 31) sbucket[warp] = inc;
+        __syncthreads();
+        int wpre = 0;
+#pragma unroll
+        for (int w = 0; w < 4; w++) wpre += (w < warp) ? sbucket[w] : 0;
+        const int T = sbucket[0] + sbucket[1] + sbucket[2] + sbucket[3];
+        sorder[threadIdx.x] = wpre + inc - cnt;           // exclusive offsets, 128 entries
+        __syncthreads();
+        if (T > 0) {
+            const int lo = (threadIdx.x * T) >> 7, hi = ((threadIdx.x + 1) * T) >> 7;
+            int todo = hi - lo;
+            int j = 0, wi = 0;
+            unsigned m = 0u;
+            float r[R::RS];
             float acc[R::V];
 #pragma unroll
-            for (int c = 0; c < C; c++) {
-                float m0 = r[6 + c * E], m1 = m0;
-                if (E == 3) {
-                    m0 = fmaf(r[6 + c * E + 1], dx, fmaf(r[6 + c * E + 2], dy0, m0));
-                    m1 = fmaf(r[6 + c * E + 1], dx, fmaf(r[6 + c * E + 2], dy1, m1));
+            for (int i = 0; i < R::V; i++) acc[i] = 0.f;
+            if (todo > 0) {
+                // last kernel whose range starts at or before lo (skips empty ones)
+                int a = 0, bnd = nb - 1;
+                while (a < bnd) {
+                    int mid = (a + bnd + 1) >> 1;
+                    if (sorder[mid] <= lo) a = mid; else bnd = mid - 1;
                 }
-                G0 = fmaf(eD0[c], m0, G0);
-                G1 = fmaf(eD1[c], m1, G1);
-                float ge0 = g0 * eD0[c], ge1 = g1 * eD1[c];
-                acc[6 + c * E] = ge0 + ge1;
-                if (E == 3) {
-                    acc[6 + c * E + 1] = (ge0 + ge1) * dx;
-                    acc[6 + c * E + 2] = fmaf(ge0, dy0, ge1 * dy1);
-                }
+                j = a;
+                int skip = lo - sorder[j];
+                m = smask[j][0];
+                while (skip >= __popc(m)) { skip -= __popc(m); m = smask[j][++wi]; }
+                for (; skip > 0; skip--) m &= m - 1;
+                load_rec(j, r);
             }
-            float sa = -0.5f * g0 * G0, sb = -0.5f * g1 * G1;
-            float sv = fmaf(sa, w0, sb * w1);
-            acc[0] = (sa + sb) * u;
-            acc[1] = sv;
-            acc[2] = (sa + sb) * u * dx;
-            acc[3] = sv * dx;
-            acc[4] = fmaf(sa * w0, dy0, sb * w1 * dy1);
-            acc[5] = sa + sb;
+            auto flush = [&](int jj) {
+                float4 *dst = reinterpret_cast<float4 *>(A.acc + (size_t)sid[jj] * R::V);
 #pragma unroll
-            for (int i = R::P; i < R::V; i++) acc[i] = 0.f;
-            int idx;
-            float tot = warp_reduce_transpose<R::V>(acc, lane, idx);
-            constexpr int GROUP = 32 / R::V;   // lanes sharing one value index
-            if ((lane & (GROUP - 1)) == 0 && idx < R::P)
-                atomicAdd(&A.acc[(size_t)sid[j] * R::V + idx], tot);
+                for (int q4 = 0; q4 < (R::P + 3) / 4; q4++)
+                    atomicAdd(dst + q4, make_float4(acc[4 * q4], acc[4 * q4 + 1], acc[4 * q4 + 2], acc[4 * q4 + 3]));
+#pragma unroll
+                for (int i = 0; i < R::V; i++) acc[i] = 0.f;
+            };
+            int got = 0;                       // pairs accumulated since the last flush
+            while (todo > 0) {
+                if (m == 0u) {
+                    if (++wi == 8) {
+                        if (got) flush(j);
+                        got = 0;
+                        ++j;
+                        wi = 0;
+                        load_rec(j, r);
+                    }
+                    m = smask[j][wi];
+                    continue;
+                }
+                const int l = __ffs(m) - 1;
+                m &= m - 1;
+                --todo;
+                ++got;
+                const int wq = wi >> 1, hh = wi & 1;
+                const int col = ((wq & 1) << 3) + (l & 7);
+                const int row = ((wq >> 1) << 3) + ((l >> 3) << 1) + hh;
+                const float4 pd = spix[(row << 4) + col];
+                const float dx = (tx0 + (float)col) - r[0], dy = (ty0f + (float)row) - r[1];
+                const float u = r[2] * dx, v = fmaf(r[3], dx, r[4] * dy);
+                const float q = fmaf(v, v, u * u);
+                const float g = ex2_approx(fmaf(q, -0.5f * LOG2E, r[5]));
+                const float ed[4] = {pd.x, pd.y, pd.z, pd.w};
+                float Gs = -ed[3];
+#pragma unroll
+                for (int c = 0; c < C; c++) {
+                    float mc = r[6 + c * E];
+                    if (E == 3) mc = fmaf(r[6 + c * E + 1], dx, fmaf(r[6 + c * E + 2], dy, mc));
+                    Gs = fmaf(ed[c], mc, Gs);
+                    const float ge = g * ed[c];
+                    acc[6 + c * E] += ge;
+                    if (E == 3) {
+                        acc[6 + c * E + 1] = fmaf(ge, dx, acc[6 + c * E + 1]);
+                        acc[6 + c * E + 2] = fmaf(ge, dy, acc[6 + c * E + 2]);
+                    }
+                }
+                const float sg = (-0.5f * g) * Gs;
+                const float su = sg * u, sv = sg * v;
+                acc[0] += su;
+                acc[1] += sv;
+                acc[2] = fmaf(su, dx, acc[2]);
+                acc[3] = fmaf(sv, dx, acc[3]);
+                acc[4] = fmaf(sv, dy, acc[4]);
+                acc[5] += sg;
+            }
+            if (got) flush(j);
         }
+        __syncthreads();
     }
 }
 
@@ -542,7 +814,7 @@ k_raster(RasterArgs A)
 // bias-corrected; clamp l11, l22 >= 1e-3.  Moments are stored
 // parameter-major m[Pk][K] so every access is coalesced.
 template <int C, int E, int MODE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(64)
 k_adam(int K, ParamsMut p, float *__restrict__ acc, const float *__restrict__ grad_in,
        float *__restrict__ grad_out, float *__restrict__ m1, float *__restrict__ m2,
        LrDev lr, HandleCtr *hc, const GridCtr *gc, long long cap)
@@ -550,33 +822,47 @@ k_adam(int K, ParamsMut p, float *__restrict__ acc, const float *__restrict__ gr
     using R = Rec<C, E>;
     constexpr int P = R::P;
     if (MODE != 2 && gc->pairs > cap) return;
-    int k = blockIdx.x * blockDim.x + threadIdx.x;
-    float g[P];
-    float mu_x = 0.f, mu_y = 0.f, l11 = 0.f, l21 = 0.f, l22 = 0.f;
-    bool live = k < K;
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = k < K;
+    const long long t = hc->t + 1;
     if (live) {
-        mu_x = p.mu[2 * k]; mu_y = p.mu[2 * k + 1];
-        l11 = p.chol[3 * k]; l21 = p.chol[3 * k + 1]; l22 = p.chol[3 * k + 2];
+        // every load first (they are independent and overlap), then compute,
+        // then every store
+        float prm[P], g[P], a1[P], a2[P];
+        {
+            float2 mu = reinterpret_cast<const float2 *>(p.mu)[k];
+            prm[0] = mu.x; prm[1] = mu.y;
+            prm[2] = p.chol[3 * k]; prm[3] = p.chol[3 * k + 1]; prm[4] = p.chol[3 * k + 2];
+            prm[5] = p.log_pi[k];
+#pragma unroll
+            for (int i = 6; i < P; i++) prm[i] = p.expert[(size_t)k * C * E + (i - 6)];
+        }
+        float raw[R::V];
         if (MODE == 2) {
 #pragma unroll
             for (int i = 0; i < P; i++) g[i] = grad_in[(size_t)k * P + i];
         } else {
-            float raw[R::V];
-            float4 *ap = reinterpret_cast<float4 *>(acc) + (size_t)k * (R::V / 4);
+            const float4 *ap = reinterpret_cast<const float4 *>(acc) + (size_t)k * (R::V / 4);
 #pragma unroll
             for (int q = 0; q < R::V / 4; q++) {
                 float4 f = ap[q];
                 raw[4 * q] = f.x; raw[4 * q + 1] = f.y; raw[4 * q + 2] = f.z; raw[4 * q + 3] = f.w;
-                ap[q] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
-            float a = 1.0f / l11, c = 1.0f / l22;
-            float b = -l21 / (l11 * l22);
+        }
+        if (MODE != 1) {
+#pragma unroll
+            for (int i = 0; i < P; i++) { a1[i] = m1[(size_t)i * K + k]; a2[i] = m2[(size_t)i * K + k]; }
+        }
+        if (MODE != 2) {
+            const float l11 = prm[2], l21 = prm[3], l22 = prm[4];
+            const float a = 1.0f / l11, c = 1.0f / l22;
+            const float b = -l21 / (l11 * l22);
             float ex_x = 0.f, ex_y = 0.f;
             if (E == 3) {
 #pragma unroll
                 for (int ch = 0; ch < C; ch++) {
-                    ex_x = fmaf(p.expert[(size_t)k * C * E + ch * E + 1], raw[6 + ch * E], ex_x);
-                    ex_y = fmaf(p.expert[(size_t)k * C * E + ch * E + 2], raw[6 + ch * E], ex_y);
+                    ex_x = fmaf(prm[6 + ch * E + 1], raw[6 + ch * E], ex_x);
+                    ex_y = fmaf(prm[6 + ch * E + 2], raw[6 + ch * E], ex_y);
                 }
             }
             g[0] = -2.f * fmaf(a, raw[0], b * raw[1]) - ex_x;
@@ -587,47 +873,42 @@ k_adam(int K, ParamsMut p, float *__restrict__ acc, const float *__restrict__ gr
             g[5] = -2.f * raw[5];
 #pragma unroll
             for (int i = 6; i < P; i++) g[i] = raw[i];
+            float4 *ap = reinterpret_cast<float4 *>(acc) + (size_t)k * (R::V / 4);
+#pragma unroll
+            for (int q = 0; q < R::V / 4; q++) ap[q] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         bool ok = true;
 #pragma unroll
         for (int i = 0; i < P; i++) ok = ok && isfinite(g[i]);
         if (!ok) atomicExch((unsigned long long *)&hc->nonfinite, 1ull);
-    }
-    if (MODE == 1) {
-        if (live) {
+        if (MODE == 1) {
 #pragma unroll
             for (int i = 0; i < P; i++) grad_out[(size_t)k * P + i] = g[i];
+        } else {
+            const float b1 = 0.9f, b2 = 0.999f, eps = 1e-8f;
+            // 1 - beta^t = -expm1(t log(beta)), accurate to a few ulp for every t
+            const float bc1 = -expm1f((float)t * log1pf(-0.1f));
+            const float bc2 = -expm1f((float)t * log1pf(-0.001f));
+#pragma unroll
+            for (int i = 0; i < P; i++) {
+                float lri = i < 2 ? lr.mu : (i < 5 ? lr.chol : (i == 5 ? lr.log_pi : (((i - 6) % E) == 0 ? lr.expert : lr.slope)));
+                a1[i] = fmaf(b1, a1[i], (1.f - b1) * g[i]);
+                a2[i] = fmaf(b2, a2[i], (1.f - b2) * g[i] * g[i]);
+                prm[i] -= lri * (a1[i] / bc1) / (sqrtf(a2[i] / bc2) + eps);
+            }
+            prm[2] = fmaxf(prm[2], 1e-3f);
+            prm[4] = fmaxf(prm[4], 1e-3f);
+#pragma unroll
+            for (int i = 0; i < P; i++) { m1[(size_t)i * K + k] = a1[i]; m2[(size_t)i * K + k] = a2[i]; }
+            reinterpret_cast<float2 *>(p.mu)[k] = make_float2(prm[0], prm[1]);
+            p.chol[3 * k] = prm[2]; p.chol[3 * k + 1] = prm[3]; p.chol[3 * k + 2] = prm[4];
+            p.log_pi[k] = prm[5];
+#pragma unroll
+            for (int i = 6; i < P; i++) p.expert[(size_t)k * C * E + (i - 6)] = prm[i];
         }
-        return;
     }
-    long long t = hc->t + 1;
-    if (live) {
-        const float b1 = 0.9f, b2 = 0.999f, eps = 1e-8f;
-        float bc1 = (float)(1.0 - pow(0.9, (double)t));
-        float bc2 = (float)(1.0 - pow(0.999, (double)t));
-        float prm[P];
-        prm[0] = mu_x; prm[1] = mu_y; prm[2] = l11; prm[3] = l21; prm[4] = l22;
-        prm[5] = p.log_pi[k];
-#pragma unroll
-        for (int i = 6; i < P; i++) prm[i] = p.expert[(size_t)k * C * E + (i - 6)];
-#pragma unroll
-        for (int i = 0; i < P; i++) {
-            float lri = i < 2 ? lr.mu : (i < 5 ? lr.chol : (i == 5 ? lr.log_pi : (((i - 6) % E) == 0 ? lr.expert : lr.slope)));
-            size_t o = (size_t)i * K + k;
-            float a1 = fmaf(b1, m1[o], (1.f - b1) * g[i]);
-            float a2 = fmaf(b2, m2[o], (1.f - b2) * g[i] * g[i]);
-            m1[o] = a1; m2[o] = a2;
-            prm[i] -= lri * (a1 / bc1) / (sqrtf(a2 / bc2) + eps);
-        }
-        prm[2] = fmaxf(prm[2], 1e-3f);
-        prm[4] = fmaxf(prm[4], 1e-3f);
-        p.mu[2 * k] = prm[0]; p.mu[2 * k + 1] = prm[1];
-        p.chol[3 * k] = prm[2]; p.chol[3 * k + 1] = prm[3]; p.chol[3 * k + 2] = prm[4];
-        p.log_pi[k] = prm[5];
-#pragma unroll
-        for (int i = 6; i < P; i++) p.expert[(size_t)k * C * E + (i - 6)] = prm[i];
-    }
-    // last CTA advances the step counter after every CTA has read it
+    if (MODE == 1) return;
+    // the last CTA advances the step counter after every CTA has read it
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();

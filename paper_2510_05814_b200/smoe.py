@@ -53,13 +53,13 @@ class c_work(ctypes.Structure):
     _fields_ = [("tested_pairs", ctypes.c_longlong), ("hit_pairs", ctypes.c_longlong)]
 
 
-KERNEL_COUNT = 7
+KERNEL_COUNT = 5
 
 
 class c_options(ctypes.Structure):
     _fields_ = [("K", ctypes.c_int), ("H", ctypes.c_int), ("W", ctypes.c_int), ("C", ctypes.c_int),
                 ("expert_order", ctypes.c_int), ("R2", ctypes.c_double), ("device", ctypes.c_int),
-                ("pair_capacity", ctypes.c_longlong)]
+                ("pair_capacity", ctypes.c_longlong), ("backward_mode", ctypes.c_int)]
 
 
 def lib():
@@ -195,7 +195,7 @@ class SMoE:
     (order 0) or linear (order 1) experts (B.json smoe_create)."""
 
     def __init__(self, K: int, H: int, W: int, C: int, expert_order: int = 0, R2: float | None = None,
-                 device: int | None = None, pair_capacity: int = 0):
+                 device: int | None = None, pair_capacity: int = 0, backward_mode: int = 0):
         L = lib()
         o = c_options()
         _check(L.smoe_default_options(ctypes.byref(o)))
@@ -204,6 +204,7 @@ class SMoE:
             o.R2 = R2
         o.device = torch.cuda.current_device() if device is None else device
         o.pair_capacity = pair_capacity
+        o.backward_mode = backward_mode
         h = ctypes.c_void_p()
         _check(L.smoe_create_ex(ctypes.byref(o), ctypes.byref(h)))
         self.h = h

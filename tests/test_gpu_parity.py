@@ -148,18 +148,36 @@ GRAD_CASES = [
 ]
 
 
+@pytest.mark.parametrize("mode", [0, 1])
 @pytest.mark.parametrize("H,W,C,K,order", GRAD_CASES)
-def test_grad_parity(H, W, C, K, order):
+def test_grad_parity(H, W, C, K, order, mode):
     pool = synth.aniso_pool(H, W, C, K, 30 + K, order=order, margin_px=5, log_pi_sd=0.4)
     pool = conditioned(pool, H, W)
     target = synth.image(H, W, C, 31 + K)
-    h = smoe.SMoE(K, H, W, C, order)
+    h = smoe.SMoE(K, H, W, C, order, backward_mode=mode)
     g, sums = h.grad(dev_pool(pool), torch.as_tensor(target).cuda())
     lg = O.loss_grad(opar(pool), target.astype(np.float64))
     s = sums.cpu().numpy()
     assert abs(s[0] - lg.sse) <= 1e-5 * lg.sse
     assert abs(s[1] - lg.sse_clamped) <= 1e-5 * lg.sse_clamped
     assert int(s[2]) == lg.uncovered
+    assert_grads(g.cpu().numpy(), lg.grad, lg.grad_abs)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_grad_parity_dense_buckets(mode):
+    """Blocks with more than one shared-memory batch (128) of kernels: the
+    backward re-derives the ellipse masks batch by batch."""
+    H, W, C, K = 40, 40, 3, 700
+    pool = synth.aniso_pool(H, W, C, K, 91, order=1, l_range=(1.5, 4.0), shear=1.5, log_pi_sd=0.3)
+    pool = conditioned(pool, H, W)
+    target = synth.image(H, W, C, 92)
+    h = smoe.SMoE(K, H, W, C, 1, backward_mode=mode)
+    rng, _, _ = h.bin(dev_pool(pool))
+    assert int((rng[1:] - rng[:-1]).max()) > 128
+    g, sums = h.grad(dev_pool(pool), torch.as_tensor(target).cuda())
+    lg = O.loss_grad(opar(pool), target.astype(np.float64))
+    assert abs(float(sums[0]) - lg.sse) <= 1e-5 * lg.sse
     assert_grads(g.cpu().numpy(), lg.grad, lg.grad_abs)
 
 
