@@ -97,12 +97,15 @@ typedef struct {
     double R2;                     /* truncation radius^2; default 2 ln 100 (Q1) */
     int device;                    /* CUDA device ordinal, -1 = current device   */
     long long pair_capacity;       /* initial pair capacity, 0 = automatic        */
-    int backward_mode;             /* 0 = kernel-parallel over ellipse masks
-                                      (default), 1 = pixel-parallel with warp
-                                      reductions                 */
+    int backward_mode;             /* 0 = pixel-parallel with warp reductions
+                                      (default), 1 = kernel-parallel over
+                                      ellipse masks              */
+    int use_graphs;                /* 1 (default): smoe_step / smoe_grad replay
+                                      their launch sequence as a CUDA graph     */
 } smoe_options;
 
-/* Fill `o` with the defaults (R2 = 2 ln 100, device = -1, automatic capacity). */
+/* Fill `o` with the defaults (R2 = 2 ln 100, device = -1, automatic capacity,
+ * pixel-parallel backward, CUDA graphs on). */
 smoe_status smoe_default_options(smoe_options *o);
 
 /* Create a handle for K kernels fitting an H x W x C image (B.json:
@@ -174,7 +177,9 @@ smoe_lr smoe_paper_lr(int t, int T);
 /* Device-time profiling of the library's own launches (bench.py uses it to
  * time the dominant kernel inside the timed region, on the handle's stream).
  * smoe_profile_begin: record a CUDA event pair around each of the next
- * max_launches launches; also count the (pixel, kernel) pairs the rasteriser
+ * max_launches launches of the kernels in kernel_mask (bit i = kernel id i,
+ * 0 = all; inside graph replays the pairs are graph event nodes); with bit
+ * SMOE_PROFILE_COUNT_WORK set the rasteriser also counts the (pixel, kernel) pairs the rasteriser
  * tests and the pairs inside the truncation ellipse (the work units of the
  * roofline).  smoe_profile_end: synchronise, return per-kernel
  * totals in times[SMOE_KERNEL_COUNT] and the work counters, stop profiling. */
@@ -186,6 +191,7 @@ enum {
     SMOE_KERNEL_ADAM = 4,          /* a8                                     */
     SMOE_KERNEL_COUNT = 5
 };
+#define SMOE_PROFILE_COUNT_WORK 0x80000000u
 typedef struct {
     double total_ms;
     long long launches;
@@ -194,7 +200,7 @@ typedef struct {
     long long tested_pairs;   /* valid pixel x listed kernel, forward sweep */
     long long hit_pairs;      /* of those, d^2 <= R2                        */
 } smoe_work;
-smoe_status smoe_profile_begin(smoe_handle h, int max_launches);
+smoe_status smoe_profile_begin(smoe_handle h, int max_launches, unsigned kernel_mask);
 smoe_status smoe_profile_end(smoe_handle h, smoe_kernel_time *times, smoe_work *work);
 const char *smoe_kernel_name(int id);
 

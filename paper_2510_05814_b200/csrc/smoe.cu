@@ -46,9 +46,52 @@ struct Ctl {
 struct Prof {
     bool on = false;
     int max = 0, n = 0;
+    unsigned mask = 0xffffffffu;     // kernels (bit = SMOE_KERNEL_*) to time
     std::vector<cudaEvent_t> ev;
     std::vector<int> kid;
     unsigned long long *d_work = nullptr;
+};
+
+// Arguments of one k_adam launch, kept so a captured graph's Adam node can
+// be re-parameterised (new learning rates) before every replay.
+struct AdamArgs {
+    int K;
+    ParamsMut pm;
+    float *acc;
+    const float *gin;
+    float *gout;
+    float *m1, *m2;
+    LrDev lr;
+    HandleCtr *hc;
+    const GridCtr *gc;
+    long long cap;
+    void *ptrs[11];
+    void bind()
+    {
+        void *a[11] = {&K, &pm, &acc, &gin, &gout, &m1, &m2, &lr, &hc, &gc, &cap};
+        for (int i = 0; i < 11; i++) ptrs[i] = a[i];
+    }
+};
+
+// A captured launch sequence (a1-a8 of smoe_step, or a1-a7 + gradient
+// finalisation of smoe_grad) replayed as one CUDA graph.
+struct StepGraph {
+    bool valid = false;
+    // key: everything baked into the captured launches
+    const void *mu = nullptr, *chol = nullptr, *lp = nullptr, *ex = nullptr, *target = nullptr, *gout = nullptr;
+    const int *ids = nullptr;
+    long long cap = 0;
+    int b0 = 0, b1 = 0, bwd = 0;
+    bool prof = false;
+    unsigned pmask = 0;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t adam = nullptr;
+    void *adam_func = nullptr;
+    dim3 adam_grid, adam_block;
+    int n_kernels = 0;
+    std::vector<cudaGraphNode_t> evA, evB;   // per timed launch, in launch order
+    std::vector<int> evk;
 };
 
 struct Grid {
@@ -80,6 +123,12 @@ struct smoe_ctx {
     long long launches = 0;
     long long init_cap = 0;
     int bwd_mode = 0;
+    bool use_graphs = true;
+    bool capturing = false;
+    cudaStream_t cap_stream = nullptr;
+    std::vector<cudaEvent_t> cap_ev;   // placeholders recorded during capture
+    std::vector<int> cap_kid;
+    StepGraph sg_step, sg_grad;
     Prof prof;
     std::string err;
 };
@@ -124,7 +173,28 @@ template <class F>
 void launch(smoe_ctx *h, int kid, const char *what, F &&f)
 {
     Prof &P = h->prof;
-    bool rec = P.on && P.n < P.max;
+    bool timed = P.on && ((P.mask >> kid) & 1u);
+    if (h->capturing) {
+        // placeholder events; every replay swaps in fresh pool events
+        int i = (int)h->cap_kid.size();
+        if (timed) {
+            while ((int)h->cap_ev.size() < 2 * (i + 1)) {
+                cudaEvent_t e;
+                CK(cudaEventCreate(&e));
+                h->cap_ev.push_back(e);
+            }
+            CK(cudaEventRecordWithFlags(h->cap_ev[2 * i], h->stream, cudaEventRecordExternal));
+        }
+        f();
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) throw SmoeError(SMOE_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+        if (timed) {
+            CK(cudaEventRecordWithFlags(h->cap_ev[2 * i + 1], h->stream, cudaEventRecordExternal));
+            h->cap_kid.push_back(kid);
+        }
+        return;
+    }
+    bool rec = timed && P.n < P.max;
     if (rec) CK(cudaEventRecord(P.ev[2 * P.n], h->stream));
     f();
     check_launch(h, what);
@@ -286,34 +356,50 @@ void forward_backward(smoe_ctx *h, const smoe_params *p, const float *target)
     A.acc = h->acc; A.dstats = h->ctl->dstats; A.out = nullptr;
     A.work = h->prof.d_work;
     launch(h, SMOE_KERNEL_RASTER_TRAIN, "k_raster<train>", [&] {
-        bool kp = h->bwd_mode == 0;
-        if (h->prof.on && kp) DISPATCH_CE(h, (k_raster<C_, E_, true, true, true><<<nt, 128, 0, h->stream>>>(A)));
+        bool kp = h->bwd_mode == 1;
+        bool cw = h->prof.on && (h->prof.mask & 0x80000000u);
+        if (cw && kp) DISPATCH_CE(h, (k_raster<C_, E_, true, true, true><<<nt, 128, 0, h->stream>>>(A)));
         else if (kp) DISPATCH_CE(h, (k_raster<C_, E_, true, false, true><<<nt, 128, 0, h->stream>>>(A)));
-        else if (h->prof.on) DISPATCH_CE(h, (k_raster<C_, E_, true, true, false><<<nt, 128, 0, h->stream>>>(A)));
+        else if (cw) DISPATCH_CE(h, (k_raster<C_, E_, true, true, false><<<nt, 128, 0, h->stream>>>(A)));
         else DISPATCH_CE(h, (k_raster<C_, E_, true, false, false><<<nt, 128, 0, h->stream>>>(A)));
     });
+}
+
+void *adam_func(smoe_ctx *h, int mode)
+{
+    void *f = nullptr;
+    if (mode == 0) DISPATCH_CE(h, (f = (void *)k_adam<C_, E_, 0>));
+    else if (mode == 1) DISPATCH_CE(h, (f = (void *)k_adam<C_, E_, 1>));
+    else DISPATCH_CE(h, (f = (void *)k_adam<C_, E_, 2>));
+    return f;
+}
+
+void adam_args(smoe_ctx *h, const smoe_params *p, const float *grad_in, float *grad_out, const smoe_lr *lr,
+               AdamArgs &a)
+{
+    a.K = h->K;
+    a.pm = ParamsMut{p->mu, p->chol, p->log_pi, p->expert};
+    a.acc = h->acc;
+    a.gin = grad_in;
+    a.gout = grad_out;
+    a.m1 = h->m1;
+    a.m2 = h->m2;
+    a.lr = lr ? LrDev{lr->mu, lr->chol, lr->log_pi, lr->expert, lr->slope} : LrDev{0, 0, 0, 0, 0};
+    a.hc = &h->ctl->hc;
+    a.gc = &h->ctl->train;
+    a.cap = h->train.cap;
+    a.bind();
 }
 
 void launch_adam(smoe_ctx *h, int mode, const smoe_params *p, const float *grad_in, float *grad_out,
                  const smoe_lr *lr)
 {
-    int K = h->K;
-    int nb = (K + 63) / 64;
-    ParamsMut pm{p->mu, p->chol, p->log_pi, p->expert};
-    LrDev l{0, 0, 0, 0, 0};
-    if (lr) l = LrDev{lr->mu, lr->chol, lr->log_pi, lr->expert, lr->slope};
-    const GridCtr *gc = &h->ctl->train;
-    long long cap = h->train.cap;
+    AdamArgs a;
+    adam_args(h, p, grad_in, grad_out, lr, a);
+    void *f = adam_func(h, mode);
+    dim3 grid((h->K + 63) / 64), block(64);
     launch(h, SMOE_KERNEL_ADAM, "k_adam", [&] {
-        if (mode == 0)
-            DISPATCH_CE(h, (k_adam<C_, E_, 0><<<nb, 64, 0, h->stream>>>(K, pm, h->acc, nullptr, nullptr, h->m1,
-                                                                           h->m2, l, &h->ctl->hc, gc, cap)));
-        else if (mode == 1)
-            DISPATCH_CE(h, (k_adam<C_, E_, 1><<<nb, 64, 0, h->stream>>>(K, pm, h->acc, nullptr, grad_out, h->m1,
-                                                                           h->m2, l, &h->ctl->hc, gc, cap)));
-        else
-            DISPATCH_CE(h, (k_adam<C_, E_, 2><<<nb, 64, 0, h->stream>>>(K, pm, h->acc, grad_in, nullptr, h->m1,
-                                                                           h->m2, l, &h->ctl->hc, gc, cap)));
+        (void)cudaLaunchKernel(f, grid, block, a.ptrs, 0, h->stream);
     });
 }
 
@@ -356,6 +442,129 @@ void fill_stats(smoe_ctx *h, smoe_stats *s)
     s->n_tiles = h->train.n_tiles;
 }
 
+void destroy_graph(StepGraph &g)
+{
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.graph) cudaGraphDestroy(g.graph);
+    g = StepGraph();
+}
+
+bool graph_matches(smoe_ctx *h, const StepGraph &g, const smoe_params *p, const float *t, float *gout)
+{
+    return g.valid && g.mu == p->mu && g.chol == p->chol && g.lp == p->log_pi && g.ex == p->expert &&
+           g.target == t && g.gout == gout && g.ids == h->train.ids && g.cap == h->train.cap &&
+           g.b0 == h->band0 && g.b1 == h->band1 &&
+           g.bwd == h->bwd_mode && g.prof == h->prof.on && g.pmask == h->prof.mask;
+}
+
+// Capture forward_backward + k_adam(mode) on the private capture stream.
+void capture(smoe_ctx *h, StepGraph &g, int mode, const smoe_params *p, const float *t, float *gout,
+             const smoe_lr *lr)
+{
+    destroy_graph(g);
+    if (!h->cap_stream) CK(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+    cudaStream_t user = h->stream;
+    h->stream = h->cap_stream;
+    h->capturing = true;
+    h->cap_kid.clear();
+    long long launches0 = h->launches;
+    cudaGraph_t graph = nullptr;
+    CK(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
+    try {
+        forward_backward(h, p, t);
+        launch_adam(h, mode, p, nullptr, gout, lr);
+    } catch (...) {
+        cudaStreamEndCapture(h->cap_stream, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        h->stream = user;
+        h->capturing = false;
+        throw;
+    }
+    cudaError_t e = cudaStreamEndCapture(h->cap_stream, &graph);
+    h->stream = user;
+    h->capturing = false;
+    h->launches = launches0;
+    if (e != cudaSuccess) throw SmoeError(SMOE_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    g.graph = graph;
+    CK(cudaGraphInstantiate(&g.exec, graph, 0));
+    size_t nn = 0;
+    CK(cudaGraphGetNodes(graph, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    CK(cudaGraphGetNodes(graph, nodes.data(), &nn));
+    size_t nt = h->cap_kid.size();
+    g.evA.assign(nt, nullptr);
+    g.evB.assign(nt, nullptr);
+    g.evk = h->cap_kid;
+    g.adam_func = adam_func(h, mode);
+    g.n_kernels = 0;
+    for (cudaGraphNode_t nd : nodes) {
+        cudaGraphNodeType ty;
+        CK(cudaGraphNodeGetType(nd, &ty));
+        if (ty == cudaGraphNodeTypeKernel) {
+            cudaKernelNodeParams kp;
+            CK(cudaGraphKernelNodeGetParams(nd, &kp));
+            g.n_kernels++;
+            if (kp.func == g.adam_func) { g.adam = nd; g.adam_grid = kp.gridDim; g.adam_block = kp.blockDim; }
+        } else if (ty == cudaGraphNodeTypeEventRecord) {
+            cudaEvent_t ev;
+            CK(cudaGraphEventRecordNodeGetEvent(nd, &ev));
+            for (size_t i = 0; i < nt; i++) {
+                if (h->cap_ev[2 * i] == ev) g.evA[i] = nd;
+                if (h->cap_ev[2 * i + 1] == ev) g.evB[i] = nd;
+            }
+        }
+    }
+    if (!g.adam) throw SmoeError(SMOE_ERR_CUDA, "graph capture: Adam node not found");
+    g.mu = p->mu; g.chol = p->chol; g.lp = p->log_pi; g.ex = p->expert;
+    g.target = t; g.gout = gout; g.ids = h->train.ids; g.cap = h->train.cap;
+    g.b0 = h->band0; g.b1 = h->band1; g.bwd = h->bwd_mode;
+    g.prof = h->prof.on; g.pmask = h->prof.mask;
+    g.valid = true;
+}
+
+// Replay: new learning rates into the Adam node, fresh profiling events, launch.
+void replay(smoe_ctx *h, StepGraph &g, const smoe_params *p, float *gout, const smoe_lr *lr)
+{
+    AdamArgs a;
+    adam_args(h, p, nullptr, gout, lr, a);
+    cudaKernelNodeParams kp = {};
+    kp.func = g.adam_func;
+    kp.gridDim = g.adam_grid;
+    kp.blockDim = g.adam_block;
+    kp.sharedMemBytes = 0;
+    kp.kernelParams = a.ptrs;
+    kp.extra = nullptr;
+    CK(cudaGraphExecKernelNodeSetParams(g.exec, g.adam, &kp));
+    Prof &P = h->prof;
+    if (g.prof) {
+        for (size_t i = 0; i < g.evk.size(); i++) {
+            if (P.n >= P.max || !g.evA[i] || !g.evB[i]) break;
+            CK(cudaGraphExecEventRecordNodeSetEvent(g.exec, g.evA[i], P.ev[2 * P.n]));
+            CK(cudaGraphExecEventRecordNodeSetEvent(g.exec, g.evB[i], P.ev[2 * P.n + 1]));
+            P.kid[P.n] = g.evk[i];
+            P.n++;
+        }
+    }
+    CK(cudaGraphLaunch(g.exec, h->stream));
+    h->launches += g.n_kernels;
+}
+
+// One step (mode 0) or gradient pass (mode 1): graph replay once the grid
+// is calibrated, eager launches otherwise.
+void run_sequence(smoe_ctx *h, int mode, const smoe_params *p, const float *t, float *gout, const smoe_lr *lr)
+{
+    StepGraph &g = mode == 0 ? h->sg_step : h->sg_grad;
+    bool ready = h->use_graphs && h->train.calibrated && h->train.oH == h->H && h->train.oW == h->W &&
+                 h->train.cnt != nullptr;
+    if (!ready) {
+        forward_backward(h, p, t);
+        launch_adam(h, mode, p, nullptr, gout, lr);
+        return;
+    }
+    if (!graph_matches(h, g, p, t, gout)) capture(h, g, mode, p, t, gout, lr);
+    replay(h, g, p, gout, lr);
+}
+
 }  // namespace
 
 // ============================================================== C ABI =====
@@ -386,6 +595,7 @@ smoe_status smoe_default_options(smoe_options *o)
     o->C = 3;
     o->R2 = 2.0 * std::log(100.0);   // chi2_2(0.99) (Q1)
     o->device = -1;
+    o->use_graphs = 1;
     return SMOE_OK;
 }
 
@@ -425,6 +635,7 @@ smoe_status smoe_create_ex(const smoe_options *o, smoe_handle *out)
     h->R2 = (float)o->R2;
     h->init_cap = o->pair_capacity;
     h->bwd_mode = o->backward_mode;
+    h->use_graphs = o->use_graphs != 0;
     int dev = o->device;
     if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) {
         (void)cudaGetLastError();
@@ -480,6 +691,10 @@ smoe_status smoe_destroy(smoe_handle h)
     dfree(h->ctl); dfree(h->stage_in); dfree(h->stage_out); dfree(h->stage_sums);
     if (h->h_ctl) cudaFreeHost(h->h_ctl);
     for (cudaEvent_t e : h->prof.ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : h->cap_ev) cudaEventDestroy(e);
+    destroy_graph(h->sg_step);
+    destroy_graph(h->sg_grad);
+    if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
     dfree(h->prof.d_work);
     (void)cudaGetLastError();
     delete h;
@@ -536,8 +751,7 @@ smoe_status smoe_step(smoe_handle h, smoe_params *p, const float *target, const 
         if (!target || !lr) throw SmoeError(SMOE_ERR_INVALID_ARG, "smoe_step: NULL target or lr");
         for (int attempt = 0;; attempt++) {
             const float *t = stage_target(h, target);
-            forward_backward(h, p, t);
-            launch_adam(h, 0, p, nullptr, nullptr, lr);
+            run_sequence(h, 0, p, t, nullptr, lr);
             if (!stats) return SMOE_OK;
             read_ctl(h);
             smoe_status st = faults(h);
@@ -558,10 +772,9 @@ smoe_status smoe_grad(smoe_handle h, const smoe_params *p, const float *target, 
         bool sdev = sums ? is_device_ptr(sums) : true;
         for (int attempt = 0;; attempt++) {
             const float *t = stage_target(h, target);
-            forward_backward(h, p, t);
             size_t n = (size_t)h->K * h->P;
             float *gout = gdev ? grad : stage(h->stage_out, h->stage_out_n, n);
-            launch_adam(h, 1, p, nullptr, gout, nullptr);
+            run_sequence(h, 1, p, t, gout, nullptr);
             if (gdev && sdev) {
                 if (sums)
                     CK(cudaMemcpyAsync(sums, h->ctl->dstats, 3 * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
@@ -622,7 +835,7 @@ smoe_status smoe_render(smoe_handle h, const smoe_params *p, int out_H, int out_
             A.R2 = h->R2; A.out = o;
             A.work = h->prof.d_work;
             launch(h, SMOE_KERNEL_RASTER_RENDER, "k_raster<render>", [&] {
-                if (h->prof.on) DISPATCH_CE(h, (k_raster<C_, E_, false, true, false><<<g.n_tiles, 128, 0, h->stream>>>(A)));
+                if (h->prof.on && (h->prof.mask & 0x80000000u)) DISPATCH_CE(h, (k_raster<C_, E_, false, true, false><<<g.n_tiles, 128, 0, h->stream>>>(A)));
                 else DISPATCH_CE(h, (k_raster<C_, E_, false, false, false><<<g.n_tiles, 128, 0, h->stream>>>(A)));
             });
             if (odev) return SMOE_OK;
@@ -680,7 +893,7 @@ const char *smoe_kernel_name(int id)
     return (id >= 0 && id < SMOE_KERNEL_COUNT) ? names[id] : "?";
 }
 
-smoe_status smoe_profile_begin(smoe_handle h, int max_launches)
+smoe_status smoe_profile_begin(smoe_handle h, int max_launches, unsigned kernel_mask)
 {
     if (!h) return SMOE_ERR_BAD_HANDLE;
     if (max_launches < 1) { set_err(h, "max_launches < 1"); return SMOE_ERR_INVALID_ARG; }
@@ -694,6 +907,7 @@ smoe_status smoe_profile_begin(smoe_handle h, int max_launches)
         P.kid.assign(max_launches, -1);
         P.max = max_launches;
         P.n = 0;
+        P.mask = kernel_mask ? kernel_mask : 0xffffffffu;
         if (!P.d_work) CK(cudaMalloc(&P.d_work, 2 * sizeof(unsigned long long)));
         CK(cudaMemsetAsync(P.d_work, 0, 2 * sizeof(unsigned long long), h->stream));
         P.on = true;

@@ -448,7 +448,7 @@ __device__ __forceinline__ float warp_reduce_transpose(float (&v)[V], int lane, 
 // Forward (a5): D = sum g, N_c = sum g m_c(x) per pixel in registers.
 // RENDER: y = N/D written to out.  TRAIN: loss partials (a6), then the
 // backward (a7) in one of two forms:
-//   KPAR = false  pixel-parallel: every warp re-sweeps K_n, per (warp,
+//   KPAR = false  pixel-parallel (default): every warp re-sweeps K_n, per (warp,
 //                 kernel) the raw gradient sums are reduced across the warp
 //                 (transpose butterfly) and added with one atomic per value.
 //   KPAR = true   kernel-parallel: the forward records, per kernel, the

@@ -59,7 +59,8 @@ KERNEL_COUNT = 5
 class c_options(ctypes.Structure):
     _fields_ = [("K", ctypes.c_int), ("H", ctypes.c_int), ("W", ctypes.c_int), ("C", ctypes.c_int),
                 ("expert_order", ctypes.c_int), ("R2", ctypes.c_double), ("device", ctypes.c_int),
-                ("pair_capacity", ctypes.c_longlong), ("backward_mode", ctypes.c_int)]
+                ("pair_capacity", ctypes.c_longlong), ("backward_mode", ctypes.c_int),
+                ("use_graphs", ctypes.c_int)]
 
 
 def lib():
@@ -92,7 +93,7 @@ def lib():
                           ctypes.POINTER(ctypes.c_longlong), P]),
         "smoe_paper_lr": (c_lr, [I, I]),
         "smoe_launch_count": (ctypes.c_longlong, [H]),
-        "smoe_profile_begin": (st, [H, I]),
+        "smoe_profile_begin": (st, [H, I, ctypes.c_uint]),
         "smoe_profile_end": (st, [H, P, ctypes.POINTER(c_work)]),
         "smoe_kernel_name": (ctypes.c_char_p, [I]),
         "smoe_status_string": (ctypes.c_char_p, [st]),
@@ -195,7 +196,8 @@ class SMoE:
     (order 0) or linear (order 1) experts (B.json smoe_create)."""
 
     def __init__(self, K: int, H: int, W: int, C: int, expert_order: int = 0, R2: float | None = None,
-                 device: int | None = None, pair_capacity: int = 0, backward_mode: int = 0):
+                 device: int | None = None, pair_capacity: int = 0, backward_mode: int = 0,
+                 use_graphs: bool = True):
         L = lib()
         o = c_options()
         _check(L.smoe_default_options(ctypes.byref(o)))
@@ -205,6 +207,7 @@ class SMoE:
         o.device = torch.cuda.current_device() if device is None else device
         o.pair_capacity = pair_capacity
         o.backward_mode = backward_mode
+        o.use_graphs = int(bool(use_graphs))
         h = ctypes.c_void_p()
         _check(L.smoe_create_ex(ctypes.byref(o), ctypes.byref(h)))
         self.h = h
@@ -298,9 +301,20 @@ class SMoE:
     def launch_count(self) -> int:
         return int(lib().smoe_launch_count(self.h))
 
-    def profile_begin(self, max_launches: int):
-        """smoe_profile_begin: time the next launches with CUDA events."""
-        _check(lib().smoe_profile_begin(self.h, int(max_launches)), self.h)
+    def profile_begin(self, max_launches: int, kernels=None, count_work: bool = False):
+        """smoe_profile_begin: time the next launches of ``kernels`` (names,
+        None = all) with CUDA event pairs on the handle's stream; with
+        ``count_work`` the raster also counts tested / hit pairs."""
+        mask = 0
+        if kernels:
+            names = [lib().smoe_kernel_name(i).decode() for i in range(KERNEL_COUNT)]
+            for k in kernels:
+                mask |= 1 << names.index(k)
+        else:
+            mask = (1 << KERNEL_COUNT) - 1
+        if count_work:
+            mask |= 0x80000000
+        _check(lib().smoe_profile_begin(self.h, int(max_launches), mask), self.h)
 
     def profile_end(self):
         """smoe_profile_end -> ({kernel name: (total_ms, launches)}, (tested, hit))."""
