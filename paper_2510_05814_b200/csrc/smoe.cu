@@ -7,7 +7,9 @@
 #include "smoe.h"
 #include "smoe_kernels.cuh"
 
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -96,7 +98,7 @@ struct StepGraph {
 
 struct Grid {
     int oH = 0, oW = 0, nx = 0, ny = 0, n_tiles = 0;
-    int *cnt = nullptr, *start = nullptr, *cursor = nullptr;
+    int *cnt = nullptr, *start = nullptr, *cursor = nullptr, *order = nullptr;
     int *ids = nullptr, *tmp = nullptr;
     long long cap = 0;
     bool calibrated = false;
@@ -123,6 +125,7 @@ struct smoe_ctx {
     long long launches = 0;
     long long init_cap = 0;
     int bwd_mode = 0;
+    int n_sm = 148;
     bool use_graphs = true;
     bool capturing = false;
     cudaStream_t cap_stream = nullptr;
@@ -224,7 +227,7 @@ void dfree(T *&p)
 
 void free_grid(Grid &g)
 {
-    dfree(g.cnt); dfree(g.start); dfree(g.cursor); dfree(g.ids); dfree(g.tmp);
+    dfree(g.cnt); dfree(g.start); dfree(g.cursor); dfree(g.order); dfree(g.ids); dfree(g.tmp);
     g = Grid();
 }
 
@@ -243,7 +246,7 @@ void ensure_grid(smoe_ctx *h, Grid &g, GridCtr *gc, int oH, int oW)
     if (g.oH == oH && g.oW == oW && g.cnt) return;
     long long cap = g.cap;
     bool cal = g.calibrated && g.oH == oH && g.oW == oW;
-    dfree(g.cnt); dfree(g.start); dfree(g.cursor);
+    dfree(g.cnt); dfree(g.start); dfree(g.cursor); dfree(g.order);
     g.oH = oH; g.oW = oW;
     g.nx = (oW + TILE - 1) / TILE;
     g.ny = (oH + TILE - 1) / TILE;
@@ -252,6 +255,7 @@ void ensure_grid(smoe_ctx *h, Grid &g, GridCtr *gc, int oH, int oW)
     CK(cudaMalloc(&g.cnt, sizeof(int) * g.n_tiles));
     CK(cudaMalloc(&g.start, sizeof(int) * (g.n_tiles + 1)));
     CK(cudaMalloc(&g.cursor, sizeof(int) * g.n_tiles));
+    CK(cudaMalloc(&g.order, sizeof(int) * g.n_tiles));
     CK(cudaMemsetAsync(g.cnt, 0, sizeof(int) * g.n_tiles, h->stream));
     CK(cudaMemsetAsync(gc, 0, sizeof(GridCtr), h->stream));
     g.cap = cap;
@@ -306,7 +310,7 @@ void bin(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_hi, bool 
         DISPATCH_CE(h, (k_preprocess<C_, E_><<<nb, PRE_NT, 0, h->stream>>>(
                            K, pdev(p), h->R2, sx, sy, g.oW, g.oH, g.nx, ty_lo, ty_hi, h->rec, h->tbox,
                            g.cnt, &h->ctl->hc, g.n_tiles, g.start, g.cursor, g.cap, g.gc,
-                           zero_stats ? h->ctl->dstats : nullptr)));
+                           zero_stats ? h->ctl->dstats : nullptr, g.order)));
     });
     if (!g.calibrated) {
         long long P;
@@ -349,6 +353,7 @@ void forward_backward(smoe_ctx *h, const smoe_params *p, const float *target)
     if (nt <= 0) return;
     RasterArgs A{};
     A.rec = h->rec; A.ids = g.ids; A.tmp = g.tmp; A.start = g.start; A.gc = g.gc; A.cap = g.cap;
+    A.order = getenv("SMOE_NO_LPT") ? nullptr : g.order; A.gcw = g.gc; A.n_work = nt; A.n_sm = h->n_sm;
     A.nx = g.nx; A.tile0 = ty_lo * g.nx; A.oW = h->W; A.oH = h->H;
     A.sx = 1.0f; A.sy = 1.0f; A.R2 = h->R2;
     A.target = target;
@@ -358,10 +363,13 @@ void forward_backward(smoe_ctx *h, const smoe_params *p, const float *target)
     launch(h, SMOE_KERNEL_RASTER_TRAIN, "k_raster<train>", [&] {
         bool kp = h->bwd_mode == 1;
         bool cw = h->prof.on && (h->prof.mask & 0x80000000u);
-        if (cw && kp) DISPATCH_CE(h, (k_raster<C_, E_, true, true, true><<<nt, 128, 0, h->stream>>>(A)));
-        else if (kp) DISPATCH_CE(h, (k_raster<C_, E_, true, false, true><<<nt, 128, 0, h->stream>>>(A)));
-        else if (cw) DISPATCH_CE(h, (k_raster<C_, E_, true, true, false><<<nt, 128, 0, h->stream>>>(A)));
-        else DISPATCH_CE(h, (k_raster<C_, E_, true, false, false><<<nt, 128, 0, h->stream>>>(A)));
+        const void *f = nullptr;
+        if (cw && kp) DISPATCH_CE(h, (f = (const void *)k_raster<C_, E_, true, true, true>));
+        else if (kp) DISPATCH_CE(h, (f = (const void *)k_raster<C_, E_, true, false, true>));
+        else if (cw) DISPATCH_CE(h, (f = (const void *)k_raster<C_, E_, true, true, false>));
+        else DISPATCH_CE(h, (f = (const void *)k_raster<C_, E_, true, false, false>));
+        void *args[1] = {&A};
+        (void)cudaLaunchKernel(f, dim3(nt), dim3(128), args, 0, h->stream);
     });
 }
 
@@ -646,6 +654,7 @@ smoe_status smoe_create_ex(const smoe_options *o, smoe_handle *out)
     h->device = dev;
     smoe_status st = guard(h, [&]() {
         size_t K = h->K;
+        CK(cudaDeviceGetAttribute(&h->n_sm, cudaDevAttrMultiProcessorCount, h->device));
         CK(cudaMalloc(&h->rec, K * h->RS * sizeof(float)));
         CK(cudaMalloc(&h->tbox, K * sizeof(int4)));
         CK(cudaMalloc(&h->acc, K * h->V * sizeof(float)));
@@ -830,13 +839,18 @@ smoe_status smoe_render(smoe_handle h, const smoe_params *p, int out_H, int out_
             float *o = odev ? out : stage(h->stage_out, h->stage_out_n, n);
             RasterArgs A{};
             A.rec = h->rec; A.ids = g.ids; A.tmp = g.tmp; A.start = g.start; A.gc = g.gc; A.cap = g.cap;
+            A.order = g.order; A.gcw = g.gc; A.n_work = g.n_tiles; A.n_sm = h->n_sm;
             A.nx = g.nx; A.tile0 = 0; A.oW = out_W; A.oH = out_H;
             A.sx = (float)h->W / (float)out_W; A.sy = (float)h->H / (float)out_H;
             A.R2 = h->R2; A.out = o;
             A.work = h->prof.d_work;
             launch(h, SMOE_KERNEL_RASTER_RENDER, "k_raster<render>", [&] {
-                if (h->prof.on && (h->prof.mask & 0x80000000u)) DISPATCH_CE(h, (k_raster<C_, E_, false, true, false><<<g.n_tiles, 128, 0, h->stream>>>(A)));
-                else DISPATCH_CE(h, (k_raster<C_, E_, false, false, false><<<g.n_tiles, 128, 0, h->stream>>>(A)));
+                const void *f = nullptr;
+                if (h->prof.on && (h->prof.mask & 0x80000000u))
+                    DISPATCH_CE(h, (f = (const void *)k_raster<C_, E_, false, true, false>));
+                else DISPATCH_CE(h, (f = (const void *)k_raster<C_, E_, false, false, false>));
+                void *args[1] = {&A};
+                (void)cudaLaunchKernel(f, dim3(g.n_tiles), dim3(128), args, 0, h->stream);
             });
             if (odev) return SMOE_OK;
             read_ctl(h);

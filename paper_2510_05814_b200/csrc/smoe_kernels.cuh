@@ -34,7 +34,7 @@ struct GridCtr {
     long long need;       // latched: largest P that exceeded the capacity
     long long skipped;    // latched: sequences skipped because of overflow
     unsigned int ticket;  // last-CTA ticket of k_preprocess
-    unsigned int pad;
+    unsigned int work;    // raster work-queue head (reset by k_preprocess)
 };
 
 // Per-handle device counters.
@@ -204,7 +204,7 @@ k_preprocess(int K, ParamsDev p, float R2, float sx /* oW/W */, float sy /* oH/H
              int nx, int ty_lo, int ty_hi, float *__restrict__ rec,
              int4 *__restrict__ tbox, int *__restrict__ cnt, HandleCtr *hc,
              int n_tiles, int *__restrict__ start, int *__restrict__ cursor, long long cap,
-             GridCtr *gc, double *dstats)
+             GridCtr *gc, double *dstats, int *__restrict__ order)
 {
     int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k < K) preprocess_one<C, E>(k, p, R2, sx, sy, oW, oH, nx, ty_lo, ty_hi, rec, tbox, cnt, hc);
@@ -219,7 +219,38 @@ k_preprocess(int K, ParamsDev p, float R2, float sx /* oW/W */, float sy /* oH/H
     if (!last) return;
     __threadfence();
     scan_counts<PRE_NT>(cnt, n_tiles, start, cursor, cap, gc, dstats);
-    if (threadIdx.x == 0) gc->ticket = 0;
+    // raster work order for the band's blocks: longest lists first (LPT),
+    // counting sort on min(|K_n|, 255)
+    __shared__ int hist[256];
+    const int t0 = ty_lo * nx, nt = (ty_hi - ty_lo) * nx;
+    hist[threadIdx.x] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < nt; i += PRE_NT) {
+        int c = start[t0 + i + 1] - start[t0 + i];
+        atomicAdd(&hist[255 - min(c, 255)], 1);
+    }
+    __syncthreads();
+    {
+        int v = hist[threadIdx.x], inc = v, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(FULL, inc, o);
+            if (lane >= o) inc += t;
+        }
+        __shared__ int wt[PRE_NT / 32];
+        if (lane == 31) wt[wid] = inc;
+        __syncthreads();
+        int pre = 0;
+        for (int w = 0; w < wid; w++) pre += wt[w];
+        hist[threadIdx.x] = pre + inc - v;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nt; i += PRE_NT) {
+        int c = start[t0 + i + 1] - start[t0 + i];
+        int pos = atomicAdd(&hist[255 - min(c, 255)], 1);
+        order[pos] = t0 + i;
+    }
+    if (threadIdx.x == 0) { gc->ticket = 0; gc->work = 0; }
 }
 
 
@@ -394,6 +425,10 @@ __device__ __forceinline__ void sort_bucket(int *seg, int n, int *tmp, int *s, i
 
 // ------------------------------------------------------- a5 / a6 / a7 -----
 struct RasterArgs {
+    const int *order;     // LPT block order (k_preprocess)
+    GridCtr *gcw;         // work-queue head
+    int n_work;           // number of blocks in the order
+    int n_sm;             // SM count (stratum width of the LPT assignment)
     const float *rec;
     int *ids;             // block lists (bucket-sorted in place by the raster)
     int *tmp;             // merge scratch for buckets larger than the smem chunk
@@ -461,8 +496,7 @@ __device__ __forceinline__ float warp_reduce_transpose(float (&v)[V], int lane, 
 // Mask bit layout: word 2w+h (warp w, h = upper/lower pixel of the lane's
 // pair), bit l = lane l: col = (w&1)*8 + (l&7), row = (w>>1)*8 + (l>>3)*2 + h.
 template <int C, int E, bool TRAIN, bool PROF, bool KPAR>
-__global__ void __launch_bounds__(128)
-k_raster(RasterArgs A)
+__device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
 {
     using R = Rec<C, E>;
     constexpr int RS4 = R::RS / 4;
@@ -475,9 +509,7 @@ k_raster(RasterArgs A)
     __shared__ int sorder[MASKS ? 128 : 1];          // per-kernel pair offsets
     __shared__ int sbucket[MASKS ? 4 : 1];           // per-warp totals
     __shared__ double red[3][4];
-    if (A.gc->pairs > A.cap) return;
 
-    const int tile = A.tile0 + blockIdx.x;
     const int tx = tile % A.nx, ty = tile / A.nx;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int px = tx * TILE + (warp & 1) * 8 + (lane & 7);
@@ -797,6 +829,22 @@ k_raster(RasterArgs A)
         }
         __syncthreads();
     }
+}
+
+// Raster grid: one CTA per block.  CTAs take the blocks in the LPT order
+// written by k_preprocess (longest K_n first), boustrophedon over strata of
+// n_sm consecutive CTAs (CTA b is placed on SM ~ b mod n_sm), so that every
+// SM receives a mix of long and short lists when the whole grid is resident,
+// and later waves start with the longest remaining lists.
+template <int C, int E, bool TRAIN, bool PROF, bool KPAR>
+__global__ void __launch_bounds__(128, KPAR ? 8 : 12)
+k_raster(RasterArgs A)
+{
+    if (A.gc->pairs > A.cap) return;
+    int i = blockIdx.x;
+    const int k = i / A.n_sm, j = i - k * A.n_sm;
+    if ((k & 1) && (k + 1) * A.n_sm <= A.n_work) i = k * A.n_sm + (A.n_sm - 1 - j);
+    raster_tile<C, E, TRAIN, PROF, KPAR>(A, A.order ? A.order[i] : A.tile0 + i);
 }
 
 // ---------------------------------------------------------------- a8 ------

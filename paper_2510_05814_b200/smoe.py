@@ -17,7 +17,7 @@ from dataclasses import dataclass
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsmoe.so")
+LIB_PATH = os.environ.get("SMOE_LIB") or os.path.join(_HERE, "libsmoe.so")   # SMOE_LIB: A/B builds
 _LIB = None
 
 OK, ERR_INVALID_ARG, ERR_CUDA, ERR_OUT_OF_MEMORY, ERR_NONFINITE, ERR_CAPACITY, ERR_BAD_HANDLE = range(7)
