@@ -100,6 +100,7 @@ struct Grid {
     int oH = 0, oW = 0, nx = 0, ny = 0, n_tiles = 0;
     int *cnt = nullptr, *start = nullptr, *cursor = nullptr, *order = nullptr;
     int *ids = nullptr, *tmp = nullptr;
+    unsigned long long *lb_state = nullptr;   // look-back scan status words
     long long cap = 0;
     bool calibrated = false;
     GridCtr *gc = nullptr;   // points into Ctl
@@ -228,6 +229,7 @@ void dfree(T *&p)
 void free_grid(Grid &g)
 {
     dfree(g.cnt); dfree(g.start); dfree(g.cursor); dfree(g.order); dfree(g.ids); dfree(g.tmp);
+    dfree(g.lb_state);
     g = Grid();
 }
 
@@ -246,7 +248,7 @@ void ensure_grid(smoe_ctx *h, Grid &g, GridCtr *gc, int oH, int oW)
     if (g.oH == oH && g.oW == oW && g.cnt) return;
     long long cap = g.cap;
     bool cal = g.calibrated && g.oH == oH && g.oW == oW;
-    dfree(g.cnt); dfree(g.start); dfree(g.cursor); dfree(g.order);
+    dfree(g.cnt); dfree(g.start); dfree(g.cursor); dfree(g.order); dfree(g.lb_state);
     g.oH = oH; g.oW = oW;
     g.nx = (oW + TILE - 1) / TILE;
     g.ny = (oH + TILE - 1) / TILE;
@@ -256,6 +258,11 @@ void ensure_grid(smoe_ctx *h, Grid &g, GridCtr *gc, int oH, int oW)
     CK(cudaMalloc(&g.start, sizeof(int) * (g.n_tiles + 1)));
     CK(cudaMalloc(&g.cursor, sizeof(int) * g.n_tiles));
     CK(cudaMalloc(&g.order, sizeof(int) * g.n_tiles));
+    if (g.n_tiles > SCAN_SINGLE_MAX) {
+        size_t nb = (g.n_tiles + LB_CHUNK - 1) / LB_CHUNK;
+        CK(cudaMalloc(&g.lb_state, sizeof(unsigned long long) * nb));
+        CK(cudaMemsetAsync(g.lb_state, 0, sizeof(unsigned long long) * nb, h->stream));
+    }
     CK(cudaMemsetAsync(g.cnt, 0, sizeof(int) * g.n_tiles, h->stream));
     CK(cudaMemsetAsync(gc, 0, sizeof(GridCtr), h->stream));
     g.cap = cap;
@@ -310,8 +317,15 @@ void bin(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_hi, bool 
         DISPATCH_CE(h, (k_preprocess<C_, E_><<<nb, PRE_NT, 0, h->stream>>>(
                            K, pdev(p), h->R2, sx, sy, g.oW, g.oH, g.nx, ty_lo, ty_hi, h->rec, h->tbox,
                            g.cnt, &h->ctl->hc, g.n_tiles, g.start, g.cursor, g.cap, g.gc,
-                           zero_stats ? h->ctl->dstats : nullptr, g.order)));
+                           zero_stats ? h->ctl->dstats : nullptr, g.lb_state ? nullptr : g.order)));
     });
+    if (g.lb_state) {
+        int nb2 = (g.n_tiles + LB_CHUNK - 1) / LB_CHUNK;
+        launch(h, SMOE_KERNEL_PREPROCESS, "k_scan_lookback", [&] {
+            k_scan_lookback<<<nb2, LB_NT, 0, h->stream>>>(g.cnt, g.n_tiles, g.start, g.cursor, g.cap, g.gc,
+                                                           zero_stats ? h->ctl->dstats : nullptr, g.lb_state);
+        });
+    }
     if (!g.calibrated) {
         long long P;
         CK(cudaMemcpyAsync(&P, &g.gc->pairs, sizeof(P), cudaMemcpyDeviceToHost, h->stream));
@@ -353,7 +367,8 @@ void forward_backward(smoe_ctx *h, const smoe_params *p, const float *target)
     if (nt <= 0) return;
     RasterArgs A{};
     A.rec = h->rec; A.ids = g.ids; A.tmp = g.tmp; A.start = g.start; A.gc = g.gc; A.cap = g.cap;
-    A.order = getenv("SMOE_NO_LPT") ? nullptr : g.order; A.gcw = g.gc; A.n_work = nt; A.n_sm = h->n_sm;
+    A.order = (getenv("SMOE_NO_LPT") || g.lb_state) ? nullptr : g.order;
+    A.gcw = g.gc; A.n_work = nt; A.n_sm = h->n_sm;
     A.nx = g.nx; A.tile0 = ty_lo * g.nx; A.oW = h->W; A.oH = h->H;
     A.sx = 1.0f; A.sy = 1.0f; A.R2 = h->R2;
     A.target = target;
@@ -839,7 +854,7 @@ smoe_status smoe_render(smoe_handle h, const smoe_params *p, int out_H, int out_
             float *o = odev ? out : stage(h->stage_out, h->stage_out_n, n);
             RasterArgs A{};
             A.rec = h->rec; A.ids = g.ids; A.tmp = g.tmp; A.start = g.start; A.gc = g.gc; A.cap = g.cap;
-            A.order = g.order; A.gcw = g.gc; A.n_work = g.n_tiles; A.n_sm = h->n_sm;
+            A.order = g.lb_state ? nullptr : g.order; A.gcw = g.gc; A.n_work = g.n_tiles; A.n_sm = h->n_sm;
             A.nx = g.nx; A.tile0 = 0; A.oW = out_W; A.oH = out_H;
             A.sx = (float)h->W / (float)out_W; A.sy = (float)h->H / (float)out_H;
             A.R2 = h->R2; A.out = o;

@@ -35,6 +35,10 @@ struct GridCtr {
     long long skipped;    // latched: sequences skipped because of overflow
     unsigned int ticket;  // last-CTA ticket of k_preprocess
     unsigned int work;    // raster work-queue head (reset by k_preprocess)
+    unsigned int scan_vid;   // k_scan_lookback: virtual CTA counter
+    unsigned int scan_done;  // k_scan_lookback: finished-CTA ticket
+    unsigned int epoch;      // k_scan_lookback: tag of the current scan
+    unsigned int pad2;
 };
 
 // Per-handle device counters.
@@ -208,6 +212,7 @@ k_preprocess(int K, ParamsDev p, float R2, float sx /* oW/W */, float sy /* oH/H
 {
     int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k < K) preprocess_one<C, E>(k, p, R2, sx, sy, oW, oH, nx, ty_lo, ty_hi, rec, tbox, cnt, hc);
+    if (!order) return;   // large grid: k_scan_lookback follows
     // the last CTA to finish scans the counts (a2)
     __shared__ bool last;
     __syncthreads();
@@ -253,6 +258,109 @@ k_preprocess(int K, ParamsDev p, float R2, float sx /* oW/W */, float sy /* oH/H
     if (threadIdx.x == 0) { gc->ticket = 0; gc->work = 0; }
 }
 
+
+// Large grids (n_tiles > SCAN_SINGLE_MAX): single-pass decoupled look-back
+// scan of the block counts, 4096 counts per CTA.  Each CTA takes a virtual
+// index from a counter (so predecessors are always resident), publishes its
+// aggregate, accumulates its predecessors' published values, publishes its
+// inclusive prefix.  Status words carry an epoch tag so nothing needs
+// clearing between scans; the last CTA to finish resets the counters.
+constexpr int SCAN_SINGLE_MAX = 32768;
+constexpr int LB_NT = 256, LB_IPT = 16, LB_CHUNK = LB_NT * LB_IPT;
+
+__device__ __forceinline__ unsigned long long lb_pack(unsigned epoch, unsigned flag, long long v)
+{
+    return ((unsigned long long)(epoch & 0xffffffu) << 40) | ((unsigned long long)flag << 38) |
+           (unsigned long long)v;
+}
+
+__global__ void __launch_bounds__(LB_NT)
+k_scan_lookback(int *__restrict__ cnt, int n, int *__restrict__ start, int *__restrict__ cursor,
+                long long cap, GridCtr *gc, double *dstats, unsigned long long *state)
+{
+    __shared__ int vid_s;
+    __shared__ unsigned epoch_s;
+    __shared__ int wtot[LB_NT / 32];
+    __shared__ long long excl_s;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) {
+        vid_s = (int)atomicAdd(&gc->scan_vid, 1u);
+        epoch_s = (*(volatile unsigned *)&gc->epoch + 1u) & 0xffffffu;
+    }
+    __syncthreads();
+    const int vid = vid_s;
+    const unsigned epoch = epoch_s;
+    if (vid == 0 && tid < 4 && dstats) dstats[tid] = 0.0;
+    const int base = vid * LB_CHUNK + tid * LB_IPT;
+    int v[LB_IPT];
+    int loc = 0;
+#pragma unroll
+    for (int q = 0; q < LB_IPT; q++) {
+        v[q] = (base + q < n) ? __ldcg(cnt + base + q) : 0;
+        loc += v[q];
+    }
+    int inc = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) wtot[wid] = inc;
+    __syncthreads();
+    int wpre = 0, agg = 0;
+#pragma unroll
+    for (int w = 0; w < LB_NT / 32; w++) {
+        wpre += (w < wid) ? wtot[w] : 0;
+        agg += wtot[w];
+    }
+    if (tid == 0) {
+        long long ex = 0;
+        if (vid == 0) {
+            atomicExch(state + vid, lb_pack(epoch, 2u, agg));
+        } else {
+            atomicExch(state + vid, lb_pack(epoch, 1u, agg));
+            for (int j = vid - 1; j >= 0;) {
+                unsigned long long sw = *(volatile unsigned long long *)(state + j);
+                if ((unsigned)(sw >> 40) != epoch || ((sw >> 38) & 3u) == 0u) continue;   // not yet published
+                ex += (long long)(sw & ((1ull << 38) - 1));
+                if (((sw >> 38) & 3u) == 2u) break;
+                j--;
+            }
+            atomicExch(state + vid, lb_pack(epoch, 2u, ex + agg));
+        }
+        excl_s = ex;
+    }
+    __syncthreads();
+    int e = (int)excl_s + wpre + inc - loc;
+#pragma unroll
+    for (int q = 0; q < LB_IPT; q++) {
+        if (base + q < n) {
+            start[base + q] = e;
+            cursor[base + q] = e;
+            cnt[base + q] = 0;
+        }
+        e += v[q];
+    }
+    const int nblk = (n + LB_CHUNK - 1) / LB_CHUNK;
+    if (tid == 0 && vid == nblk - 1) {
+        long long P = excl_s + agg;
+        start[n] = (int)P;
+        gc->pairs = P;
+        if (P > cap) {
+            if (P > gc->need) gc->need = P;
+            gc->skipped += 1;
+        }
+    }
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(&gc->scan_done, 1u) == (unsigned)nblk - 1) {
+            gc->scan_vid = 0;
+            gc->scan_done = 0;
+            gc->epoch = epoch;
+            __threadfence();
+        }
+    }
+}
 
 // ---------------------------------------------------------------- a3 ------
 // First radix digit: every block b_n inside kernel k's box records k

@@ -88,6 +88,33 @@ def test_binning_large_bucket_merge_path():
     np.testing.assert_array_equal(ids.numpy(), ids_ref)
 
 
+def test_large_grid_lookback_scan_and_render():
+    """An output raster with more than 32768 blocks takes the multi-CTA
+    look-back scan (and the identity block order); lists stay bit-exact and
+    sampled pixels match the oracle."""
+    H, W, C, K = 1456, 1456, 3, 300
+    oH = oW = 2912                       # 182 x 182 = 33124 blocks
+    pool = synth.aniso_pool(H, W, C, K, 61, order=1, margin_px=4)
+    pool = conditioned(pool, H, W, oH, oW)
+    h = smoe.SMoE(K, H, W, C, 1)
+    p = dev_pool(pool)
+    rng, ids, tb = h.bin(p, oH, oW)
+    _, tb_ref, _ = O.boxes(opar(pool), H, W, oH, oW)
+    rng_ref, ids_ref = O.tile_list(tb_ref, 182, 182)
+    np.testing.assert_array_equal(rng.numpy(), rng_ref)
+    np.testing.assert_array_equal(ids.numpy(), ids_ref)
+    y = h.render(p, oH, oW).cpu().numpy()
+    g = np.random.default_rng(3)
+    ix, iy = g.integers(0, oW, 2000), g.integers(0, oH, 2000)
+    xs = (ix + 0.5) * W / oW - 0.5
+    ys = (iy + 0.5) * H / oH - 0.5
+    y_ref, _ = O.render_points(opar(pool), xs, ys)
+    assert_pixels(y[:, iy, ix].T, y_ref)
+    # and a training step on the small grid still works after the big render
+    st = h.step(p, torch.as_tensor(synth.image(H, W, C, 62)).cuda(), smoe.LR())
+    assert np.isfinite(st.loss)
+
+
 def test_binning_empty_and_outside():
     H, W = 40, 40
     pool = synth.aniso_pool(H, W, 1, 10, 3)
