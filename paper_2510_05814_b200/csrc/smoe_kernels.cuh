@@ -612,10 +612,9 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
     constexpr bool MASKS = TRAIN && KPAR;
     __shared__ float4 srec[BATCH * RS4];
     __shared__ int sid[BATCH];
-    __shared__ unsigned smask[MASKS ? BATCH : 1][8];
     __shared__ float4 spix[MASKS ? 256 : 1];      // eD_0..eD_{C-1}, K  (C <= 3)
-    __shared__ int sorder[MASKS ? 128 : 1];          // per-kernel pair offsets
-    __shared__ int sbucket[MASKS ? 4 : 1];           // per-warp totals
+    constexpr int CAPW = 2048;                    // per-warp pair-list capacity (window)
+    __shared__ unsigned short spw[MASKS ? 4 : 1][MASKS ? CAPW : 1];   // (kernel << 8) | pixel
     __shared__ double red[3][4];
 
     const int tx = tile % A.nx, ty = tile / A.nx;
@@ -632,10 +631,13 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
     constexpr int SCHUNK = (BATCH * RS4 * 4 >= 2048) ? 2048 : 1024;
     sort_bucket(A.ids + s0, n, A.tmp + s0, reinterpret_cast<int *>(srec), SCHUNK);
 
-    float D0 = 0.f, D1 = 0.f, N0[C], N1[C];
+    float2 D2 = make_float2(0.f, 0.f), N2[C];
 #pragma unroll
-    for (int c = 0; c < C; c++) N0[c] = N1[c] = 0.f;
+    for (int c = 0; c < C; c++) N2[c] = make_float2(0.f, 0.f);
     unsigned long long w_tested = 0, w_hit = 0;
+    int wrun = 0;                                  // pairs this warp listed (KPAR)
+    const unsigned lt = (1u << lane) - 1u;
+    const int pix0 = ((warp >> 1) * 8 + (lane >> 3) * 2) * 16 + (warp & 1) * 8 + (lane & 7);
     const int w_valid = PROF ? __popc(__ballot_sync(FULL, v0)) + __popc(__ballot_sync(FULL, v1)) : 0;
 
     auto load_batch = [&](int b0, int nb) {
@@ -656,13 +658,17 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
         }
     };
     // d^2 of this lane's two pixels for record r
-    auto dist2 = [&](const float (&r)[R::RS], float &dx, float &dy0, float &dy1, float &u, float &w0,
-                     float &w1, float &q0, float &q1) {
-        dx = xs - r[0]; dy0 = ys0 - r[1]; dy1 = ys1 - r[1];
+    // The lane's two pixels share dx and differ in dy: their arithmetic is
+    // done pairwise with packed f32x2 instructions (FADD2/FMUL2/FFMA2, sm_100).
+    const float2 ys2 = make_float2(ys0, ys1);
+    auto dist2 = [&](const float (&r)[R::RS], float &dx, float2 &dy, float &u, float2 &w, float2 &q) {
+        dx = xs - r[0];
+        dy = __fadd2_rn(ys2, make_float2(-r[1], -r[1]));
         u = r[2] * dx;
-        w0 = fmaf(r[3], dx, r[4] * dy0); w1 = fmaf(r[3], dx, r[4] * dy1);
-        float uu = u * u;
-        q0 = fmaf(w0, w0, uu); q1 = fmaf(w1, w1, uu);
+        const float bdx = r[3] * dx;
+        w = __ffma2_rn(make_float2(r[4], r[4]), dy, make_float2(bdx, bdx));
+        const float uu = u * u;
+        q = __ffma2_rn(w, w, make_float2(uu, uu));
     };
 
     // ---- forward (Eq. 5 with the per-pixel cull of P:221) ----
@@ -672,28 +678,35 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
         for (int j = 0; j < nb; j++) {
             float r[R::RS];
             load_rec(j, r);
-            float dx, dy0, dy1, u, w0, w1, q0, q1;
-            dist2(r, dx, dy0, dy1, u, w0, w1, q0, q1);
-            bool h0 = v0 && q0 <= R2, h1 = v1 && q1 <= R2;
+            float dx, u;
+            float2 dy, w, q;
+            dist2(r, dx, dy, u, w, q);
+            bool h0 = v0 && q.x <= R2, h1 = v1 && q.y <= R2;
             unsigned b0m = __ballot_sync(FULL, h0), b1m = __ballot_sync(FULL, h1);
             if (PROF) {
                 w_tested += w_valid;
                 w_hit += __popc(b0m) + __popc(b1m);
             }
-            if (MASKS && lane == 0 && n <= BATCH) { smask[j][2 * warp] = b0m; smask[j][2 * warp + 1] = b1m; }
             if ((b0m | b1m) == 0u) continue;
-            float g0 = h0 ? ex2_approx(fmaf(q0, -0.5f * LOG2E, r[5])) : 0.f;
-            float g1 = h1 ? ex2_approx(fmaf(q1, -0.5f * LOG2E, r[5])) : 0.f;
-            D0 += g0; D1 += g1;
+            if (MASKS && n <= BATCH) {
+                // this warp's pairs of kernel j, appended to its list
+                const int c0 = __popc(b0m);
+                const int p0 = wrun + __popc(b0m & lt), p1 = wrun + c0 + __popc(b1m & lt);
+                if (h0 && p0 < CAPW) spw[warp][p0] = (unsigned short)((j << 8) | pix0);
+                if (h1 && p1 < CAPW) spw[warp][p1] = (unsigned short)((j << 8) | (pix0 + 16));
+                wrun += c0 + __popc(b1m);
+            }
+            const float2 ea = __ffma2_rn(q, make_float2(-0.5f * LOG2E, -0.5f * LOG2E), make_float2(r[5], r[5]));
+            const float2 g = make_float2(h0 ? ex2_approx(ea.x) : 0.f, h1 ? ex2_approx(ea.y) : 0.f);
+            D2 = __fadd2_rn(D2, g);
 #pragma unroll
             for (int c = 0; c < C; c++) {
-                float m0 = r[6 + c * E], m1 = m0;
+                float2 m = make_float2(r[6 + c * E], r[6 + c * E]);
                 if (E == 3) {
-                    m0 = fmaf(r[6 + c * E + 1], dx, fmaf(r[6 + c * E + 2], dy0, m0));
-                    m1 = fmaf(r[6 + c * E + 1], dx, fmaf(r[6 + c * E + 2], dy1, m1));
+                    const float mb = fmaf(r[6 + c * E + 1], dx, r[6 + c * E]);
+                    m = __ffma2_rn(make_float2(r[6 + c * E + 2], r[6 + c * E + 2]), dy, make_float2(mb, mb));
                 }
-                N0[c] = fmaf(g0, m0, N0[c]);
-                N1[c] = fmaf(g1, m1, N1[c]);
+                N2[c] = __ffma2_rn(g, m, N2[c]);
             }
         }
     }
@@ -701,10 +714,11 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
         atomicAdd(&A.work[0], w_tested);
         atomicAdd(&A.work[1], w_hit);
     }
+    const float D0 = D2.x, D1 = D2.y;
     float y0[C], y1[C];
     float iD0 = D0 > 0.f ? 1.0f / D0 : 0.f, iD1 = D1 > 0.f ? 1.0f / D1 : 0.f;
 #pragma unroll
-    for (int c = 0; c < C; c++) { y0[c] = N0[c] * iD0; y1[c] = N1[c] * iD1; }
+    for (int c = 0; c < C; c++) { y0[c] = N2[c].x * iD0; y1[c] = N2[c].y * iD1; }
 
     if (!TRAIN) {
         size_t plane = (size_t)A.oH * A.oW;
@@ -768,8 +782,10 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
             for (int j = 0; j < nb; j++) {
                 float r[R::RS];
                 load_rec(j, r);
-                float dx, dy0, dy1, u, w0, w1, q0, q1;
-                dist2(r, dx, dy0, dy1, u, w0, w1, q0, q1);
+                float dx, u;
+                float2 dyv, wv, qv;
+                dist2(r, dx, dyv, u, wv, qv);
+                const float dy0 = dyv.x, dy1 = dyv.y, w0 = wv.x, w1 = wv.y, q0 = qv.x, q1 = qv.y;
                 bool h0 = v0 && q0 <= R2 && D0 > 0.f, h1 = v1 && q1 <= R2 && D1 > 0.f;
                 if (!__any_sync(FULL, h0 || h1)) continue;
                 float g0 = h0 ? ex2_approx(fmaf(q0, -0.5f * LOG2E, r[5])) : 0.f;
@@ -812,104 +828,70 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
         return;
     }
 
-    // ---- kernel-parallel backward over the recorded ellipse masks ----
-    // The batch's (kernel, masked pixel) pairs, kernel-major, are split into
-    // 128 equal contiguous ranges, one per thread: every lane walks the same
-    // number of pairs (balanced), accumulates the raw sums of the current
-    // kernel in registers and flushes them with vector atomics when its range
-    // crosses into the next kernel and at the end.
+    // ---- kernel-parallel backward over per-warp pair lists ----
+    // Each warp owns the (kernel, pixel) pairs of its 8x8 quadrant that lie
+    // inside the kernel's ellipse, listed kernel-major in shared memory (the
+    // forward wrote them while testing; larger K_n rebuild them per batch).
+    // The warp's 32 lanes split the list into equal contiguous ranges, so
+    // every lane carries the same number of pairs; a lane accumulates the
+    // raw sums of the current kernel in registers and flushes them with
+    // vector atomics when the kernel changes and at the end of its range.
     const float tx0 = (float)(tx * TILE), ty0f = (float)(ty * TILE);
     for (int b0 = 0; b0 < n; b0 += BATCH) {
         int nb = min(BATCH, n - b0);
-        if (n > BATCH) {
-            // masks were not kept: reload the batch and redo the cull test
-            load_batch(b0, nb);
-            for (int j = 0; j < nb; j++) {
-                float r[R::RS];
-                load_rec(j, r);
-                float dx, dy0, dy1, u, w0, w1, q0, q1;
-                dist2(r, dx, dy0, dy1, u, w0, w1, q0, q1);
-                unsigned b0m = __ballot_sync(FULL, v0 && q0 <= R2), b1m = __ballot_sync(FULL, v1 && q1 <= R2);
-                if (lane == 0) { smask[j][2 * warp] = b0m; smask[j][2 * warp + 1] = b1m; }
+        int total = wrun;                      // n <= BATCH: listed by the forward
+        if (n > BATCH) load_batch(b0, nb);
+        for (int q0 = 0; q0 < total || (n > BATCH && q0 == 0); q0 += CAPW) {
+            if (n > BATCH || q0 > 0) {
+                // (re)build the warp's list window [q0, q0 + CAPW) for the
+                // resident batch: the cull test again, pairs in window kept
+                int run = 0;
+                for (int j = 0; j < nb; j++) {
+                    float rb[R::RS];
+                    load_rec(j, rb);
+                    float dx, u;
+                    float2 dyv, wv, qv;
+                    dist2(rb, dx, dyv, u, wv, qv);
+                    bool h0 = v0 && qv.x <= R2, h1 = v1 && qv.y <= R2;
+                    unsigned b0m = __ballot_sync(FULL, h0), b1m = __ballot_sync(FULL, h1);
+                    int p0 = run + __popc(b0m & lt) - q0, p1 = run + __popc(b0m) + __popc(b1m & lt) - q0;
+                    if (h0 && p0 >= 0 && p0 < CAPW) spw[warp][p0] = (unsigned short)((j << 8) | pix0);
+                    if (h1 && p1 >= 0 && p1 < CAPW) spw[warp][p1] = (unsigned short)((j << 8) | (pix0 + 16));
+                    run += __popc(b0m) + __popc(b1m);
+                }
+                total = run;
+                __syncwarp();
             }
-            __syncthreads();
-        }
-        // exclusive scan of the per-kernel masked-pixel counts
-        int cnt = 0;
-        if (threadIdx.x < nb) {
-#pragma unroll
-            for (int w = 0; w < 8; w++) cnt += __popc(smask[threadIdx.x][w]);
-        }
-        int inc = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int t = __shfl_up_sync(FULL, inc, o);
-            if (lane >= o) inc += t;
-        }
-        if (lane == 31) sbucket[warp] = inc;
-        __syncthreads();
-        int wpre = 0;
-#pragma unroll
-        for (int w = 0; w < 4; w++) wpre += (w < warp) ? sbucket[w] : 0;
-        const int T = sbucket[0] + sbucket[1] + sbucket[2] + sbucket[3];
-        sorder[threadIdx.x] = wpre + inc - cnt;           // exclusive offsets, 128 entries
-        __syncthreads();
-        if (T > 0) {
-            const int lo = (threadIdx.x * T) >> 7, hi = ((threadIdx.x + 1) * T) >> 7;
-            int todo = hi - lo;
-            int j = 0, wi = 0;
-            unsigned m = 0u;
+            if (q0 >= total) break;
+            const int Tw = min(total - q0, CAPW);
+            const int lo = (lane * Tw) >> 5, hi = ((lane + 1) * Tw) >> 5;
+            int cj = -1;
+            float4 *dst = nullptr;
             float r[R::RS];
             float acc[R::V];
 #pragma unroll
             for (int i = 0; i < R::V; i++) acc[i] = 0.f;
-            if (todo > 0) {
-                // last kernel whose range starts at or before lo (skips empty ones)
-                int a = 0, bnd = nb - 1;
-                while (a < bnd) {
-                    int mid = (a + bnd + 1) >> 1;
-                    if (sorder[mid] <= lo) a = mid; else bnd = mid - 1;
-                }
-                j = a;
-                int skip = lo - sorder[j];
-                m = smask[j][0];
-                while (skip >= __popc(m)) { skip -= __popc(m); m = smask[j][++wi]; }
-                for (; skip > 0; skip--) m &= m - 1;
-                load_rec(j, r);
-            }
-            auto flush = [&](int jj) {
-                float4 *dst = reinterpret_cast<float4 *>(A.acc + (size_t)sid[jj] * R::V);
+            for (int q = lo; q < hi; q++) {
+                const unsigned e = spw[warp][q];
+                const int j = (int)(e >> 8), pix = (int)(e & 255u);
+                if (j != cj) {
+                    if (cj >= 0) {
 #pragma unroll
-                for (int q4 = 0; q4 < (R::P + 3) / 4; q4++)
-                    atomicAdd(dst + q4, make_float4(acc[4 * q4], acc[4 * q4 + 1], acc[4 * q4 + 2], acc[4 * q4 + 3]));
+                        for (int q4 = 0; q4 < (R::P + 3) / 4; q4++)
+                            atomicAdd(dst + q4, make_float4(acc[4 * q4], acc[4 * q4 + 1], acc[4 * q4 + 2], acc[4 * q4 + 3]));
 #pragma unroll
-                for (int i = 0; i < R::V; i++) acc[i] = 0.f;
-            };
-            int got = 0;                       // pairs accumulated since the last flush
-            while (todo > 0) {
-                if (m == 0u) {
-                    if (++wi == 8) {
-                        if (got) flush(j);
-                        got = 0;
-                        ++j;
-                        wi = 0;
-                        load_rec(j, r);
+                        for (int i = 0; i < R::V; i++) acc[i] = 0.f;
                     }
-                    m = smask[j][wi];
-                    continue;
+                    cj = j;
+                    dst = reinterpret_cast<float4 *>(A.acc + (size_t)sid[j] * R::V);
+                    load_rec(j, r);
                 }
-                const int l = __ffs(m) - 1;
-                m &= m - 1;
-                --todo;
-                ++got;
-                const int wq = wi >> 1, hh = wi & 1;
-                const int col = ((wq & 1) << 3) + (l & 7);
-                const int row = ((wq >> 1) << 3) + ((l >> 3) << 1) + hh;
-                const float4 pd = spix[(row << 4) + col];
+                const int col = pix & 15, row = pix >> 4;
+                const float4 pd = spix[pix];
                 const float dx = (tx0 + (float)col) - r[0], dy = (ty0f + (float)row) - r[1];
                 const float u = r[2] * dx, v = fmaf(r[3], dx, r[4] * dy);
-                const float q = fmaf(v, v, u * u);
-                const float g = ex2_approx(fmaf(q, -0.5f * LOG2E, r[5]));
+                const float qd = fmaf(v, v, u * u);
+                const float g = ex2_approx(fmaf(qd, -0.5f * LOG2E, r[5]));
                 const float ed[4] = {pd.x, pd.y, pd.z, pd.w};
                 float Gs = -ed[3];
 #pragma unroll
@@ -933,7 +915,12 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
                 acc[4] = fmaf(sv, dy, acc[4]);
                 acc[5] += sg;
             }
-            if (got) flush(j);
+            if (cj >= 0) {
+#pragma unroll
+                for (int q4 = 0; q4 < (R::P + 3) / 4; q4++)
+                    atomicAdd(dst + q4, make_float4(acc[4 * q4], acc[4 * q4 + 1], acc[4 * q4 + 2], acc[4 * q4 + 3]));
+            }
+            __syncwarp();
         }
         __syncthreads();
     }
