@@ -163,7 +163,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
-    ap.add_argument("--backward-mode", type=int, default=0, help="0 pixel-parallel (default), 1 kernel-parallel")
+    ap.add_argument("--backward-mode", type=int, default=-1, help="-1 auto (default), 0 pixel-parallel, 1 kernel-parallel")
     ap.add_argument("--no-profile", action="store_true", help="no per-kernel events in the timed region")
     args = ap.parse_args()
     assert args.warmup >= 3, "at least 3 warm-up steps"

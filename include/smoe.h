@@ -97,15 +97,16 @@ typedef struct {
     double R2;                     /* truncation radius^2; default 2 ln 100 (Q1) */
     int device;                    /* CUDA device ordinal, -1 = current device   */
     long long pair_capacity;       /* initial pair capacity, 0 = automatic        */
-    int backward_mode;             /* 0 = pixel-parallel with warp reductions
-                                      (default), 1 = kernel-parallel over
-                                      ellipse masks              */
+    int backward_mode;             /* -1 = auto (default: kernel-parallel unless
+                                      blocks average > 110 kernels), 0 = pixel-
+                                      parallel with warp reductions, 1 = kernel-
+                                      parallel over per-warp pair lists (§5)   */
     int use_graphs;                /* 1 (default): smoe_step / smoe_grad replay
                                       their launch sequence as a CUDA graph     */
 } smoe_options;
 
 /* Fill `o` with the defaults (R2 = 2 ln 100, device = -1, automatic capacity,
- * pixel-parallel backward, CUDA graphs on). */
+ * automatic backward form, CUDA graphs on). */
 smoe_status smoe_default_options(smoe_options *o);
 
 /* Create a handle for K kernels fitting an H x W x C image (B.json:

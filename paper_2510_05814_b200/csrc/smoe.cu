@@ -125,7 +125,8 @@ struct smoe_ctx {
     int band0 = 0, band1 = 0;   // tile rows; band1 == 0 -> whole image
     long long launches = 0;
     long long init_cap = 0;
-    int bwd_mode = 0;
+    int bwd_mode = -1;          // -1 auto, 0 pixel-parallel, 1 kernel-parallel
+    double last_pairs = -1.0;   // host view of P on the training grid (last sync)
     int n_sm = 148;
     bool use_graphs = true;
     bool capturing = false;
@@ -284,6 +285,19 @@ void read_ctl(smoe_ctx *h)
 {
     CK(cudaMemcpyAsync(h->h_ctl, h->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
+    if (h->h_ctl->train.pairs > 0) h->last_pairs = (double)h->h_ctl->train.pairs;
+}
+
+// Backward form: the kernel-parallel pass over per-warp pair
+// lists wins while blocks are sparse; with long lists (denser than ~110
+// kernels per block on average, e.g. config 4) the pixel-parallel pass with
+// warp reductions is faster.  Auto mode decides from the last observed P.
+int effective_bwd(smoe_ctx *h)
+{
+    if (h->bwd_mode >= 0) return h->bwd_mode;
+    double nt = (double)((h->H + TILE - 1) / TILE) * ((h->W + TILE - 1) / TILE);
+    if (h->last_pairs < 0) return 1;
+    return h->last_pairs / nt > 110.0 ? 0 : 1;
 }
 
 #define DISPATCH_CE(h, BODY)                                                  \
@@ -330,6 +344,7 @@ void bin(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_hi, bool 
         long long P;
         CK(cudaMemcpyAsync(&P, &g.gc->pairs, sizeof(P), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
+        if (&g == &h->train) h->last_pairs = (double)P;
         grow(h, g, P > h->init_cap ? P : h->init_cap);
     }
     int ns = (K + 63) / 64;
@@ -376,7 +391,7 @@ void forward_backward(smoe_ctx *h, const smoe_params *p, const float *target)
     A.acc = h->acc; A.dstats = h->ctl->dstats; A.out = nullptr;
     A.work = h->prof.d_work;
     launch(h, SMOE_KERNEL_RASTER_TRAIN, "k_raster<train>", [&] {
-        bool kp = h->bwd_mode == 1;
+        bool kp = effective_bwd(h) == 1;
         bool cw = h->prof.on && (h->prof.mask & 0x80000000u);
         const void *f = nullptr;
         if (cw && kp) DISPATCH_CE(h, (f = (const void *)k_raster<C_, E_, true, true, true>));
@@ -477,7 +492,7 @@ bool graph_matches(smoe_ctx *h, const StepGraph &g, const smoe_params *p, const 
     return g.valid && g.mu == p->mu && g.chol == p->chol && g.lp == p->log_pi && g.ex == p->expert &&
            g.target == t && g.gout == gout && g.ids == h->train.ids && g.cap == h->train.cap &&
            g.b0 == h->band0 && g.b1 == h->band1 &&
-           g.bwd == h->bwd_mode && g.prof == h->prof.on && g.pmask == h->prof.mask;
+           g.bwd == effective_bwd(h) && g.prof == h->prof.on && g.pmask == h->prof.mask;
 }
 
 // Capture forward_backward + k_adam(mode) on the private capture stream.
@@ -540,7 +555,7 @@ void capture(smoe_ctx *h, StepGraph &g, int mode, const smoe_params *p, const fl
     if (!g.adam) throw SmoeError(SMOE_ERR_CUDA, "graph capture: Adam node not found");
     g.mu = p->mu; g.chol = p->chol; g.lp = p->log_pi; g.ex = p->expert;
     g.target = t; g.gout = gout; g.ids = h->train.ids; g.cap = h->train.cap;
-    g.b0 = h->band0; g.b1 = h->band1; g.bwd = h->bwd_mode;
+    g.b0 = h->band0; g.b1 = h->band1; g.bwd = effective_bwd(h);
     g.prof = h->prof.on; g.pmask = h->prof.mask;
     g.valid = true;
 }
@@ -619,6 +634,7 @@ smoe_status smoe_default_options(smoe_options *o)
     o->R2 = 2.0 * std::log(100.0);   // chi2_2(0.99) (Q1)
     o->device = -1;
     o->use_graphs = 1;
+    o->backward_mode = -1;
     return SMOE_OK;
 }
 
@@ -640,7 +656,7 @@ smoe_status smoe_create_ex(const smoe_options *o, smoe_handle *out)
     *out = nullptr;
     if (o->K < 1 || o->H < 1 || o->W < 1 || !(o->C == 1 || o->C == 3) ||
         !(o->expert_order == 0 || o->expert_order == 1) || !(o->R2 > 0) ||
-        !(o->backward_mode == 0 || o->backward_mode == 1)) {
+        !(o->backward_mode >= -1 && o->backward_mode <= 1)) {
         g_err = "smoe_create: need K,H,W >= 1, C in {1,3}, expert_order in {0,1}, R2 > 0";
         return SMOE_ERR_INVALID_ARG;
     }

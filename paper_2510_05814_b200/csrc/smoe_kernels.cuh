@@ -868,57 +868,84 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
             int cj = -1;
             float4 *dst = nullptr;
             float r[R::RS];
-            float acc[R::V];
+            // two list entries of the same kernel per iteration, as a packed
+            // f32x2 pair (the second slot is a null pixel, eD = K = 0, when
+            // the next entry is past the range or of another kernel)
+            float2 acc[R::P];
 #pragma unroll
-            for (int i = 0; i < R::V; i++) acc[i] = 0.f;
-            for (int q = lo; q < hi; q++) {
+            for (int i = 0; i < R::P; i++) acc[i] = make_float2(0.f, 0.f);
+            for (int q = lo; q < hi;) {
                 const unsigned e = spw[warp][q];
-                const int j = (int)(e >> 8), pix = (int)(e & 255u);
+                const int j = (int)(e >> 8), pa = (int)(e & 255u);
                 if (j != cj) {
                     if (cj >= 0) {
 #pragma unroll
-                        for (int q4 = 0; q4 < (R::P + 3) / 4; q4++)
-                            atomicAdd(dst + q4, make_float4(acc[4 * q4], acc[4 * q4 + 1], acc[4 * q4 + 2], acc[4 * q4 + 3]));
+                        for (int q4 = 0; q4 < (R::P + 3) / 4; q4++) {
+                            float t4[4];
 #pragma unroll
-                        for (int i = 0; i < R::V; i++) acc[i] = 0.f;
+                            for (int k4 = 0; k4 < 4; k4++)
+                                t4[k4] = (4 * q4 + k4 < R::P) ? acc[4 * q4 + k4].x + acc[4 * q4 + k4].y : 0.f;
+                            atomicAdd(dst + q4, make_float4(t4[0], t4[1], t4[2], t4[3]));
+                        }
+#pragma unroll
+                        for (int i = 0; i < R::P; i++) acc[i] = make_float2(0.f, 0.f);
                     }
                     cj = j;
                     dst = reinterpret_cast<float4 *>(A.acc + (size_t)sid[j] * R::V);
                     load_rec(j, r);
                 }
-                const int col = pix & 15, row = pix >> 4;
-                const float4 pd = spix[pix];
-                const float dx = (tx0 + (float)col) - r[0], dy = (ty0f + (float)row) - r[1];
-                const float u = r[2] * dx, v = fmaf(r[3], dx, r[4] * dy);
-                const float qd = fmaf(v, v, u * u);
-                const float g = ex2_approx(fmaf(qd, -0.5f * LOG2E, r[5]));
-                const float ed[4] = {pd.x, pd.y, pd.z, pd.w};
-                float Gs = -ed[3];
+                unsigned e2 = (q + 1 < hi) ? spw[warp][q + 1] : 0xffffu;
+                const bool two = (int)(e2 >> 8) == j;
+                const int pb = two ? (int)(e2 & 255u) : pa;
+                q += two ? 2 : 1;
+                const float4 pda = spix[pa];
+                float4 pdb = spix[pb];
+                if (!two) pdb = make_float4(0.f, 0.f, 0.f, 0.f);
+                const float2 x2 = make_float2(tx0 + (float)(pa & 15), tx0 + (float)(pb & 15));
+                const float2 y2 = make_float2(ty0f + (float)(pa >> 4), ty0f + (float)(pb >> 4));
+                const float2 dx = __fadd2_rn(x2, make_float2(-r[0], -r[0]));
+                const float2 dy = __fadd2_rn(y2, make_float2(-r[1], -r[1]));
+                const float2 u = __fmul2_rn(make_float2(r[2], r[2]), dx);
+                const float2 v = __ffma2_rn(make_float2(r[3], r[3]), dx, __fmul2_rn(make_float2(r[4], r[4]), dy));
+                const float2 qd = __ffma2_rn(v, v, __fmul2_rn(u, u));
+                const float2 ea = __ffma2_rn(qd, make_float2(-0.5f * LOG2E, -0.5f * LOG2E), make_float2(r[5], r[5]));
+                const float2 g = make_float2(ex2_approx(ea.x), ex2_approx(ea.y));
+                const float2 eda[4] = {make_float2(pda.x, pdb.x), make_float2(pda.y, pdb.y),
+                                       make_float2(pda.z, pdb.z), make_float2(pda.w, pdb.w)};
+                float2 Gs = make_float2(-eda[3].x, -eda[3].y);
 #pragma unroll
                 for (int c = 0; c < C; c++) {
-                    float mc = r[6 + c * E];
-                    if (E == 3) mc = fmaf(r[6 + c * E + 1], dx, fmaf(r[6 + c * E + 2], dy, mc));
-                    Gs = fmaf(ed[c], mc, Gs);
-                    const float ge = g * ed[c];
-                    acc[6 + c * E] += ge;
+                    float2 mc = make_float2(r[6 + c * E], r[6 + c * E]);
                     if (E == 3) {
-                        acc[6 + c * E + 1] = fmaf(ge, dx, acc[6 + c * E + 1]);
-                        acc[6 + c * E + 2] = fmaf(ge, dy, acc[6 + c * E + 2]);
+                        mc = __ffma2_rn(make_float2(r[6 + c * E + 1], r[6 + c * E + 1]), dx, mc);
+                        mc = __ffma2_rn(make_float2(r[6 + c * E + 2], r[6 + c * E + 2]), dy, mc);
+                    }
+                    Gs = __ffma2_rn(eda[c], mc, Gs);
+                    const float2 ge = __fmul2_rn(g, eda[c]);
+                    acc[6 + c * E] = __fadd2_rn(acc[6 + c * E], ge);
+                    if (E == 3) {
+                        acc[6 + c * E + 1] = __ffma2_rn(ge, dx, acc[6 + c * E + 1]);
+                        acc[6 + c * E + 2] = __ffma2_rn(ge, dy, acc[6 + c * E + 2]);
                     }
                 }
-                const float sg = (-0.5f * g) * Gs;
-                const float su = sg * u, sv = sg * v;
-                acc[0] += su;
-                acc[1] += sv;
-                acc[2] = fmaf(su, dx, acc[2]);
-                acc[3] = fmaf(sv, dx, acc[3]);
-                acc[4] = fmaf(sv, dy, acc[4]);
-                acc[5] += sg;
+                const float2 sg = __fmul2_rn(__fmul2_rn(make_float2(-0.5f, -0.5f), g), Gs);
+                const float2 su = __fmul2_rn(sg, u), sv = __fmul2_rn(sg, v);
+                acc[0] = __fadd2_rn(acc[0], su);
+                acc[1] = __fadd2_rn(acc[1], sv);
+                acc[2] = __ffma2_rn(su, dx, acc[2]);
+                acc[3] = __ffma2_rn(sv, dx, acc[3]);
+                acc[4] = __ffma2_rn(sv, dy, acc[4]);
+                acc[5] = __fadd2_rn(acc[5], sg);
             }
             if (cj >= 0) {
 #pragma unroll
-                for (int q4 = 0; q4 < (R::P + 3) / 4; q4++)
-                    atomicAdd(dst + q4, make_float4(acc[4 * q4], acc[4 * q4 + 1], acc[4 * q4 + 2], acc[4 * q4 + 3]));
+                for (int q4 = 0; q4 < (R::P + 3) / 4; q4++) {
+                    float t4[4];
+#pragma unroll
+                    for (int k4 = 0; k4 < 4; k4++)
+                        t4[k4] = (4 * q4 + k4 < R::P) ? acc[4 * q4 + k4].x + acc[4 * q4 + k4].y : 0.f;
+                    atomicAdd(dst + q4, make_float4(t4[0], t4[1], t4[2], t4[3]));
+                }
             }
             __syncwarp();
         }
@@ -932,7 +959,7 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
 // SM receives a mix of long and short lists when the whole grid is resident,
 // and later waves start with the longest remaining lists.
 template <int C, int E, bool TRAIN, bool PROF, bool KPAR>
-__global__ void __launch_bounds__(128, KPAR ? 8 : 12)
+__global__ void __launch_bounds__(128, KPAR ? 6 : 12)
 k_raster(RasterArgs A)
 {
     if (A.gc->pairs > A.cap) return;

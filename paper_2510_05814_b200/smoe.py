@@ -196,7 +196,7 @@ class SMoE:
     (order 0) or linear (order 1) experts (B.json smoe_create)."""
 
     def __init__(self, K: int, H: int, W: int, C: int, expert_order: int = 0, R2: float | None = None,
-                 device: int | None = None, pair_capacity: int = 0, backward_mode: int = 0,
+                 device: int | None = None, pair_capacity: int = 0, backward_mode: int = -1,
                  use_graphs: bool = True):
         L = lib()
         o = c_options()
