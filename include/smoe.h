@@ -103,6 +103,13 @@ typedef struct {
                                       parallel over per-warp pair lists (§5)   */
     int use_graphs;                /* 1 (default): smoe_step / smoe_grad replay
                                       their launch sequence as a CUDA graph     */
+    int head;                      /* regression head: 0 = SMoE soft gates
+                                      (Eq. 2/4, default); 1 = RBF weighted sum
+                                      of kernels y = sum_j m_j(x) pi_j K_j(x)
+                                      (Eq. 1; GaussianImage-style,
+                                      SURVEY §8(f) f2).  R2 = INFINITY gives the
+                                      dense global (untruncated) model (GSMoE,
+                                      P:173-180).                               */
 } smoe_options;
 
 /* Fill `o` with the defaults (R2 = 2 ln 100, device = -1, automatic capacity,
@@ -127,6 +134,17 @@ smoe_status smoe_set_stream(smoe_handle h, void *stream);
  * not touch Adam state.  `out` may be host (call returns after the copy and
  * capacity check) or device (asynchronous). */
 smoe_status smoe_render(smoe_handle h, const smoe_params *p, int out_H, int out_W, float *out);
+
+/* Render options.  sharpen = s in (0, 1]: native sharpening
+ * by kernel editing, "reducing the bandwidths of the kernels by a sharpening
+ * factor": the render uses Sigma_j -> s Sigma_j (every
+ * Cholesky factor times sqrt(s)); s = 1 is the plain render.  The
+ * caller's parameters are not modified. */
+typedef struct {
+    float sharpen;
+} smoe_render_options;
+smoe_status smoe_render_ex(smoe_handle h, const smoe_params *p, int out_H, int out_W, float *out,
+                           const smoe_render_options *opt);
 
 /* One training iteration (B.json smoe_step(params, target, lr)): forward,
  * MSE loss, analytic gradients of all kernel parameters, fused Adam update

@@ -70,6 +70,8 @@ def _lib():
         lib.oracle_grad_kernels.argtypes = [I, I, I, P, P, P, P, I, I, P, D, I, P, P, P]
         lib.oracle_margins.restype = None
         lib.oracle_margins.argtypes = [I, P, P, D, I, I, I, I, P, P]
+        lib.oracle_set_head.restype = None
+        lib.oracle_set_head.argtypes = [I]
         _LIB = lib
     return _LIB
 
@@ -80,6 +82,29 @@ def _f64(a):
 
 def _ptr(a):
     return a.ctypes.data_as(ctypes.c_void_p)
+
+
+class head:
+    """Context manager selecting the regression head of the dense oracle:
+    "smoe" (Eq. 2/4, default) or "rbf" (Eq. 1, P:119-122)."""
+
+    def __init__(self, name: str):
+        self.v = {"smoe": 0, "rbf": 1}[name]
+
+    def __enter__(self):
+        _lib().oracle_set_head(self.v)
+        return self
+
+    def __exit__(self, *a):
+        _lib().oracle_set_head(0)
+
+
+def sharpened(p: "Params", s: float) -> "Params":
+    """Kernel editing for sharpening: Sigma -> s Sigma,
+    i.e. every Cholesky factor times sqrt(s); centres, gates, experts kept."""
+    q = p.copy()
+    q.chol = q.chol * np.sqrt(s)
+    return q
 
 
 def R2_99() -> float:

@@ -146,7 +146,14 @@ void oracle_gates(int K, const double *mu, const double *chol, const double *log
     if (D_out) *D_out = D;
 }
 
-/* y(x) of Eq. (2)/(5) at one source-space point, all C channels. */
+/* Regression head: 0 = SMoE, y = sum_j m_j(x) w_j(x) with the soft gates of
+ * Eq. (4) (Eq. 2); 1 = RBF / GaussianImage-style weighted sum of
+ * kernels y = sum_j m_j(x) pi_j K_j(x) (Eq. 1; pi_j = 1 there, kept
+ * as a multiplier here so log_pi = 0 reproduces Eq. 1 exactly). */
+static int g_head = 0;
+void oracle_set_head(int head) { g_head = head; }
+
+/* y(x) of Eq. (2)/(5) (or Eq. 1) at one source-space point, all C channels. */
 static void eval_point(int K, int C, int order, const double *mu, const double *chol,
                        const double *log_pi, const double *expert,
                        double px, double py, double R2, double *y, double *D_out)
@@ -162,7 +169,8 @@ static void eval_point(int K, int C, int order, const double *mu, const double *
         for (int c = 0; c < C; c++)
             y[c] += g * expert_value(expert + (size_t)(j * C + c) * E, order, dx, dy);
     }
-    for (int c = 0; c < C; c++) y[c] = D > 0.0 ? y[c] / D : 0.0;  /* Q7 */
+    if (g_head == 0)
+        for (int c = 0; c < C; c++) y[c] = D > 0.0 ? y[c] / D : 0.0;  /* Q7 */
     if (D_out) *D_out = D;
 }
 
@@ -219,11 +227,13 @@ static void add_pair_grad(int C, int order, const double *mu, const double *chol
     oracle_cov(chol, &s11, &s12, &s22);
     double det = s11 * s22 - s12 * s12;
     double q1 = (s22 * dx - s12 * dy) / det, q2 = (-s12 * dx + s11 * dy) / det;
-    double w = gn / D;
+    /* SMoE: dy_c/dg_j = (m_jc(x) - y_c)/D, dy_c/dm_jc(x) = w_j = g_j/D;
+     * RBF (Eq. 1): dy_c/dg_j = m_jc(x), dy_c/dm_jc(x) = g_j. */
+    double w = g_head == 0 ? gn / D : gn;
     double G = 0.0;
     for (int c = 0; c < C; c++)
-        G += ev[c] * (expert_value(e_j + c * E, order, dx, dy) - yv[c]);
-    G /= D;
+        G += ev[c] * (expert_value(e_j + c * E, order, dx, dy) - (g_head == 0 ? yv[c] : 0.0));
+    if (g_head == 0) G /= D;
     double s = -0.5 * gn * G;
     double l11 = chol[0], l21 = chol[1], l22 = chol[2];
     double t[64];

@@ -128,6 +128,7 @@ struct smoe_ctx {
     int bwd_mode = -1;          // -1 auto, 0 pixel-parallel, 1 kernel-parallel
     double last_pairs = -1.0;   // host view of P on the training grid (last sync)
     int n_sm = 148;
+    int head = 0;               // 0 SMoE (Eq. 2/4), 1 RBF (Eq. 1)
     bool use_graphs = true;
     bool capturing = false;
     cudaStream_t cap_stream = nullptr;
@@ -322,7 +323,7 @@ void check_params(const smoe_params *p)
 // a1-a4: preprocess, scan, scatter, in-bucket sort on grid g for block rows
 // [ty_lo, ty_hi).  The first binning of a grid calibrates the capacity with
 // one synchronous read of P; later binnings never synchronise.
-void bin(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_hi, bool zero_stats)
+void bin(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_hi, bool zero_stats, float lscale = 1.0f)
 {
     int K = h->K;
     int nb = (K + PRE_NT - 1) / PRE_NT;
@@ -331,7 +332,7 @@ void bin(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_hi, bool 
         DISPATCH_CE(h, (k_preprocess<C_, E_><<<nb, PRE_NT, 0, h->stream>>>(
                            K, pdev(p), h->R2, sx, sy, g.oW, g.oH, g.nx, ty_lo, ty_hi, h->rec, h->tbox,
                            g.cnt, &h->ctl->hc, g.n_tiles, g.start, g.cursor, g.cap, g.gc,
-                           zero_stats ? h->ctl->dstats : nullptr, g.lb_state ? nullptr : g.order)));
+                           zero_stats ? h->ctl->dstats : nullptr, g.lb_state ? nullptr : g.order, lscale)));
     });
     if (g.lb_state) {
         int nb2 = (g.n_tiles + LB_CHUNK - 1) / LB_CHUNK;
@@ -385,7 +386,7 @@ void forward_backward(smoe_ctx *h, const smoe_params *p, const float *target)
     A.order = (getenv("SMOE_NO_LPT") || g.lb_state) ? nullptr : g.order;
     A.gcw = g.gc; A.n_work = nt; A.n_sm = h->n_sm;
     A.nx = g.nx; A.tile0 = ty_lo * g.nx; A.oW = h->W; A.oH = h->H;
-    A.sx = 1.0f; A.sy = 1.0f; A.R2 = h->R2;
+    A.sx = 1.0f; A.sy = 1.0f; A.R2 = h->R2; A.rbf = h->head;
     A.target = target;
     A.e_scale = (float)(2.0 / ((double)h->H * h->W * h->C));
     A.acc = h->acc; A.dstats = h->ctl->dstats; A.out = nullptr;
@@ -656,7 +657,7 @@ smoe_status smoe_create_ex(const smoe_options *o, smoe_handle *out)
     *out = nullptr;
     if (o->K < 1 || o->H < 1 || o->W < 1 || !(o->C == 1 || o->C == 3) ||
         !(o->expert_order == 0 || o->expert_order == 1) || !(o->R2 > 0) ||
-        !(o->backward_mode >= -1 && o->backward_mode <= 1)) {
+        !(o->backward_mode >= -1 && o->backward_mode <= 1) || !(o->head == 0 || o->head == 1)) {
         g_err = "smoe_create: need K,H,W >= 1, C in {1,3}, expert_order in {0,1}, R2 > 0";
         return SMOE_ERR_INVALID_ARG;
     }
@@ -674,6 +675,7 @@ smoe_status smoe_create_ex(const smoe_options *o, smoe_handle *out)
     h->R2 = (float)o->R2;
     h->init_cap = o->pair_capacity;
     h->bwd_mode = o->backward_mode;
+    h->head = o->head;
     h->use_graphs = o->use_graphs != 0;
     int dev = o->device;
     if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) {
@@ -856,16 +858,26 @@ smoe_status smoe_apply(smoe_handle h, smoe_params *p, const float *grad, const s
 
 smoe_status smoe_render(smoe_handle h, const smoe_params *p, int out_H, int out_W, float *out)
 {
+    return smoe_render_ex(h, p, out_H, out_W, out, nullptr);
+}
+
+smoe_status smoe_render_ex(smoe_handle h, const smoe_params *p, int out_H, int out_W, float *out,
+                           const smoe_render_options *opt)
+{
     if (!h) return SMOE_ERR_BAD_HANDLE;
     return guard(h, [&]() -> smoe_status {
         check_params(p);
         if (!out || out_H < 1 || out_W < 1 || (long long)out_H * out_W >= (1ll << 31))
             throw SmoeError(SMOE_ERR_INVALID_ARG, "smoe_render: bad output");
+        float sharpen = opt ? opt->sharpen : 1.0f;
+        if (!(sharpen > 0.0f && sharpen <= 1.0f))
+            throw SmoeError(SMOE_ERR_INVALID_ARG, "smoe_render: sharpen must be in (0, 1]");
+        float lscale = sqrtf(sharpen);
         bool odev = is_device_ptr(out);
         for (int attempt = 0;; attempt++) {
             Grid &g = h->render;
             ensure_grid(h, g, &h->ctl->render, out_H, out_W);
-            bin(h, g, p, 0, g.ny, false);
+            bin(h, g, p, 0, g.ny, false, lscale);
             size_t n = (size_t)h->C * out_H * out_W;
             float *o = odev ? out : stage(h->stage_out, h->stage_out_n, n);
             RasterArgs A{};
@@ -873,7 +885,7 @@ smoe_status smoe_render(smoe_handle h, const smoe_params *p, int out_H, int out_
             A.order = g.lb_state ? nullptr : g.order; A.gcw = g.gc; A.n_work = g.n_tiles; A.n_sm = h->n_sm;
             A.nx = g.nx; A.tile0 = 0; A.oW = out_W; A.oH = out_H;
             A.sx = (float)h->W / (float)out_W; A.sy = (float)h->H / (float)out_H;
-            A.R2 = h->R2; A.out = o;
+            A.R2 = h->R2; A.out = o; A.rbf = h->head;
             A.work = h->prof.d_work;
             launch(h, SMOE_KERNEL_RASTER_RENDER, "k_raster<render>", [&] {
                 const void *f = nullptr;

@@ -157,11 +157,12 @@ template <int C, int E>
 __device__ __forceinline__ void
 preprocess_one(int k, ParamsDev p, float R2, float sx, float sy, int oW, int oH,
                int nx, int ty_lo, int ty_hi, float *__restrict__ rec,
-               int4 *__restrict__ tbox, int *__restrict__ cnt, HandleCtr *hc)
+               int4 *__restrict__ tbox, int *__restrict__ cnt, HandleCtr *hc, float lscale)
 {
     using R = Rec<C, E>;
     float2 mu = reinterpret_cast<const float2 *>(p.mu)[k];
-    float l11 = p.chol[3 * k], l21 = p.chol[3 * k + 1], l22 = p.chol[3 * k + 2];
+    // lscale = sqrt(s) applies the sharpening edit Sigma -> s Sigma (render only)
+    float l11 = p.chol[3 * k] * lscale, l21 = p.chol[3 * k + 1] * lscale, l22 = p.chol[3 * k + 2] * lscale;
     float lp = p.log_pi[k];
     float a = 1.0f / l11, c = 1.0f / l22;
     float b = -l21 / (l11 * l22);
@@ -208,10 +209,10 @@ k_preprocess(int K, ParamsDev p, float R2, float sx /* oW/W */, float sy /* oH/H
              int nx, int ty_lo, int ty_hi, float *__restrict__ rec,
              int4 *__restrict__ tbox, int *__restrict__ cnt, HandleCtr *hc,
              int n_tiles, int *__restrict__ start, int *__restrict__ cursor, long long cap,
-             GridCtr *gc, double *dstats, int *__restrict__ order)
+             GridCtr *gc, double *dstats, int *__restrict__ order, float lscale)
 {
     int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < K) preprocess_one<C, E>(k, p, R2, sx, sy, oW, oH, nx, ty_lo, ty_hi, rec, tbox, cnt, hc);
+    if (k < K) preprocess_one<C, E>(k, p, R2, sx, sy, oW, oH, nx, ty_lo, ty_hi, rec, tbox, cnt, hc, lscale);
     if (!order) return;   // large grid: k_scan_lookback follows
     // the last CTA to finish scans the counts (a2)
     __shared__ bool last;
@@ -547,6 +548,7 @@ struct RasterArgs {
     int oW, oH;
     float sx, sy;        // source spacing of output samples: x = (j+1/2) sx - 1/2
     float R2;
+    int rbf;              // 1: RBF head y = sum_j m_j(x) pi_j K_j (Eq. 1), no gate normalisation
     // training
     const float *target; // [C][H][W] (H = oH, W = oW in training)
     float e_scale;        // 2 / (H W C): dL/dy = e_scale (y - t)
@@ -716,7 +718,8 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
     }
     const float D0 = D2.x, D1 = D2.y;
     float y0[C], y1[C];
-    float iD0 = D0 > 0.f ? 1.0f / D0 : 0.f, iD1 = D1 > 0.f ? 1.0f / D1 : 0.f;
+    // SMoE (Eq. 2/4): y = N/D.  RBF head (Eq. 1): y = N, i.e. "D" = 1.
+    float iD0 = A.rbf ? 1.f : (D0 > 0.f ? 1.0f / D0 : 0.f), iD1 = A.rbf ? 1.f : (D1 > 0.f ? 1.0f / D1 : 0.f);
 #pragma unroll
     for (int c = 0; c < C; c++) { y0[c] = N2[c].x * iD0; y1[c] = N2[c].y * iD1; }
 
@@ -748,8 +751,10 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
             ssec += (double)(rc0 * rc0) + (double)(rc1 * rc1);
             eD0[c] = A.e_scale * r0 * iD0;      // 0 if uncovered
             eD1[c] = A.e_scale * r1 * iD1;
-            K0 = fmaf(eD0[c], y0[c], K0);
-            K1 = fmaf(eD1[c], y1[c], K1);
+            if (!A.rbf) {                       // RBF: dy/dg = m(x), no -y term
+                K0 = fmaf(eD0[c], y0[c], K0);
+                K1 = fmaf(eD1[c], y1[c], K1);
+            }
         }
         unc = (double)((v0 && D0 <= 0.f) ? 1 : 0) + (double)((v1 && D1 <= 0.f) ? 1 : 0);
 #pragma unroll

@@ -60,7 +60,11 @@ class c_options(ctypes.Structure):
     _fields_ = [("K", ctypes.c_int), ("H", ctypes.c_int), ("W", ctypes.c_int), ("C", ctypes.c_int),
                 ("expert_order", ctypes.c_int), ("R2", ctypes.c_double), ("device", ctypes.c_int),
                 ("pair_capacity", ctypes.c_longlong), ("backward_mode", ctypes.c_int),
-                ("use_graphs", ctypes.c_int)]
+                ("use_graphs", ctypes.c_int), ("head", ctypes.c_int)]
+
+
+class c_render_options(ctypes.Structure):
+    _fields_ = [("sharpen", ctypes.c_float)]
 
 
 def lib():
@@ -83,6 +87,7 @@ def lib():
         "smoe_destroy": (st, [H]),
         "smoe_set_stream": (st, [H, P]),
         "smoe_render": (st, [H, ctypes.POINTER(c_params), I, I, P]),
+        "smoe_render_ex": (st, [H, ctypes.POINTER(c_params), I, I, P, ctypes.POINTER(c_render_options)]),
         "smoe_step": (st, [H, ctypes.POINTER(c_params), P, ctypes.POINTER(c_lr), ctypes.POINTER(c_stats)]),
         "smoe_set_band": (st, [H, I, I]),
         "smoe_grad": (st, [H, ctypes.POINTER(c_params), P, P, P]),
@@ -197,7 +202,7 @@ class SMoE:
 
     def __init__(self, K: int, H: int, W: int, C: int, expert_order: int = 0, R2: float | None = None,
                  device: int | None = None, pair_capacity: int = 0, backward_mode: int = -1,
-                 use_graphs: bool = True):
+                 use_graphs: bool = True, head: str = "smoe"):
         L = lib()
         o = c_options()
         _check(L.smoe_default_options(ctypes.byref(o)))
@@ -208,6 +213,7 @@ class SMoE:
         o.pair_capacity = pair_capacity
         o.backward_mode = backward_mode
         o.use_graphs = int(bool(use_graphs))
+        o.head = {"smoe": 0, "rbf": 1}[head]
         h = ctypes.c_void_p()
         _check(L.smoe_create_ex(ctypes.byref(o), ctypes.byref(h)))
         self.h = h
@@ -245,14 +251,18 @@ class SMoE:
         _check(lib().smoe_step(self.h, ctypes.byref(p), _ptr(target), ctypes.byref(lr.c()), None), self.h)
         return None
 
-    def render(self, params: Params, out_H: int | None = None, out_W: int | None = None, out=None):
-        """smoe_render: y on an out_H x out_W raster -> [C, out_H, out_W]."""
+    def render(self, params: Params, out_H: int | None = None, out_W: int | None = None, out=None,
+               sharpen: float = 1.0):
+        """smoe_render(_ex): y on an out_H x out_W raster -> [C, out_H, out_W];
+        ``sharpen`` = s < 1 renders with Sigma -> s Sigma (kernel editing)."""
         self._stream()
         out_H = self.H if out_H is None else out_H
         out_W = self.W if out_W is None else out_W
         if out is None:
             out = torch.empty((self.C, out_H, out_W), dtype=torch.float32, device=f"cuda:{self.device}")
-        _check(lib().smoe_render(self.h, ctypes.byref(params.c()), out_H, out_W, _ptr(out)), self.h)
+        ro = c_render_options(sharpen)
+        _check(lib().smoe_render_ex(self.h, ctypes.byref(params.c()), out_H, out_W, _ptr(out), ctypes.byref(ro)),
+               self.h)
         return out
 
     def set_band(self, tile_row0: int, tile_row1: int):

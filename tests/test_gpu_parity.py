@@ -376,3 +376,63 @@ def test_kodak_full_size_sampled_parity():
     sel = g.choice(K, 16, replace=False)
     g_ref, a_ref = O.grad_kernels(op, target.astype(np.float64), sel)
     assert_grads(grad.cpu().numpy()[sel], g_ref, a_ref)
+
+
+# -------------------------------------------- NEXT rows f1 / f2 on the GPU --
+
+@pytest.mark.parametrize("scale,s", [(1.0, 0.5), (2.0, 0.25), (3.0, 0.7)])
+def test_sharpened_render_parity(scale, s):
+    """f1: native sharpening by kernel editing: the render
+    with Sigma -> s Sigma equals the oracle render of the edited kernels."""
+    H, W, C, K = 40, 44, 3, 80
+    oH, oW = int(H * scale), int(W * scale)
+    pool = synth.aniso_pool(H, W, C, K, 90, order=1, margin_px=4)
+    sharp = pool.copy()
+    sharp.chol = (sharp.chol.astype(np.float64) * np.sqrt(s)).astype(np.float32)
+    sharp = conditioned(sharp, H, W, oH, oW)
+    base = sharp.copy()
+    base.chol = (sharp.chol.astype(np.float64) / np.sqrt(s)).astype(np.float32)
+    h = smoe.SMoE(K, H, W, C, 1)
+    y = h.render(dev_pool(base), oH, oW, sharpen=s).cpu().numpy()
+    y_ref, _ = O.render(O.sharpened(opar(base), s), H, W, oH, oW)
+    assert_pixels(y, y_ref, rel=2e-5, abs_=2e-6)
+    with pytest.raises(smoe.SmoeError):
+        h.render(dev_pool(base), oH, oW, sharpen=1.5)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("C,order", [(1, 0), (3, 1)])
+def test_rbf_head_parity(C, order, mode):
+    """f2: RBF / GaussianImage-style head (Eq. 1): render and gradients."""
+    H, W, K = 36, 40, 60
+    pool = synth.aniso_pool(H, W, C, K, 95 + C, order=order, margin_px=4, log_pi_sd=0.3)
+    pool.expert[:, :, 0] *= 0.3          # keep sums of overlapping kernels moderate
+    pool = conditioned(pool, H, W)
+    target = synth.image(H, W, C, 96)
+    h = smoe.SMoE(K, H, W, C, order, head="rbf", backward_mode=mode)
+    y = h.render(dev_pool(pool)).cpu().numpy()
+    g, sums = h.grad(dev_pool(pool), torch.as_tensor(target).cuda())
+    with O.head("rbf"):
+        y_ref, _ = O.render(opar(pool), H, W)
+        lg = O.loss_grad(opar(pool), target.astype(np.float64))
+    assert_pixels(y, y_ref)
+    assert abs(float(sums[0]) - lg.sse) <= 1e-5 * lg.sse
+    assert_grads(g.cpu().numpy(), lg.grad, lg.grad_abs)
+
+
+def test_dense_global_model_parity():
+    """f2: R2 = inf is the dense global (untruncated) SMoE model of the
+    paper's GSMoE baseline: every kernel is listed in every
+    block; render and gradients match the oracle's untruncated mode."""
+    H, W, C, K = 32, 40, 3, 24
+    pool = synth.aniso_pool(H, W, C, K, 97, order=1, log_pi_sd=0.3)
+    target = synth.image(H, W, C, 98)
+    h = smoe.SMoE(K, H, W, C, 1, R2=float("inf"))
+    st = h.step(dev_pool(pool), torch.as_tensor(target).cuda(), smoe.LR(0, 0, 0, 0, 0))
+    assert st.pairs == K * 6      # 2 x 3 blocks, every kernel in each
+    y = h.render(dev_pool(pool)).cpu().numpy()
+    y_ref, _ = O.render(opar(pool), H, W, R2=float("inf"))
+    assert_pixels(y, y_ref)
+    g, _ = h.grad(dev_pool(pool), torch.as_tensor(target).cuda())
+    lg = O.loss_grad(opar(pool), target.astype(np.float64), R2=float("inf"))
+    assert_grads(g.cpu().numpy(), lg.grad, lg.grad_abs)

@@ -489,3 +489,58 @@ def test_fit_constant_target_single_kernel():
     q, trace = O.fit(p, t, 100)
     assert trace[-1][0] < 1e-6
     assert trace[-1][0] < trace[0][0]
+
+
+# ------------------------------------------------ NEXT rows f1, f2 (oracle) --
+
+def test_rbf_head_spec_and_closed_form():
+    """Eq. (1): y = sum_j m_j K_j(x).  S:142: one kernel m = 0.8,
+    Sigma = I: 0.8 at mu and 0.8 exp(-1/2) one pixel away."""
+    p = params([[5.0, 5.0]], [[1, 0, 1]], [[0.8]])
+    with O.head("rbf"):
+        y, _ = O.render_points(p, [5.0, 6.0], [5.0, 5.0])
+    assert abs(y[0, 0] - 0.8) < 1e-15
+    assert abs(y[1, 0] - 0.8 * math.exp(-0.5)) < 1e-15
+    assert abs(y[1, 0] - 0.48522) < 5e-6                         # printed value, S:142
+    # two overlapping kernels simply add (no normalisation, unlike Eq. 4)
+    p2 = params([[5.0, 5.0], [6.0, 5.0]], [[1, 0, 1]] * 2, [[0.3], [0.5]])
+    with O.head("rbf"):
+        y2, _ = O.render_points(p2, [5.5], [5.0])
+    assert abs(y2[0, 0] - 0.8 * math.exp(-0.125)) < 1e-15
+
+
+@pytest.mark.parametrize("C,order", [(1, 0), (3, 1)])
+def test_rbf_gradient_central_fd(C, order):
+    H, W = 18, 21
+    pool = synth.aniso_pool(H, W, C, 8, seed=70 + C, order=order, log_pi_sd=0.3, l_range=(2.0, 5.0))
+    pool = conditioned(pool, H, W, tau_d=1e-3)
+    p = pool_params(pool)
+    t = synth.image(H, W, C, 71).astype(np.float64)
+    with O.head("rbf"):
+        lg = O.loss_grad(p, t)
+        scale = np.abs(lg.grad).max()
+        for k in range(p.K):
+            for i in range(p.Pk):
+                fd = fd_grad(p, t, k, i)
+                assert abs(lg.grad[k, i] - fd) <= 1e-5 * abs(fd) + 1e-7 * scale, (k, i)
+
+
+def test_sharpening_spec_examples():
+    """Kernel editing: Sigma -> s Sigma.  s = 1 is the
+    identity; s = 1/4 halves every box side exactly; gates stay a partition
+    of unity; a constant-expert model stays exactly constant where covered."""
+    H, W = 30, 34
+    pool = synth.aniso_pool(H, W, 1, 20, seed=80)
+    p = pool_params(pool)
+    np.testing.assert_array_equal(O.sharpened(p, 1.0).chol, p.chol)
+    _, _, hs = O.boxes(p, H, W)
+    _, _, hs4 = O.boxes(O.sharpened(p, 0.25), H, W)
+    np.testing.assert_allclose(hs4, hs / 2, rtol=1e-15)
+    q = O.sharpened(p, 0.3)
+    for (x, y) in [(3.2, 4.1), (17.0, 15.5), (30.3, 2.2)]:
+        w, D = O.gates(q, x, y)
+        if D > 0:
+            assert abs(w.sum() - 1) < 1e-12
+    q.expert[:] = 0.625
+    yq, Dq = O.render(q, H, W, 60, 68)
+    assert np.all(np.abs(yq[0][Dq > 0] - 0.625) < 1e-15)
