@@ -143,6 +143,48 @@ def run_reference(args):
     return 0
 
 
+def run_mm(args):
+    """MM-RSMoE: H hypotheses of the config's (noisy) image fitted
+    concurrently on one GPU, fused by averaging (Eq. 11).  Reports hypothesis
+    iterations/s over the timed fit and the PSNR of single vs fused models
+    against the clean image."""
+    import numpy as np
+    import torch
+    from paper_2510_05814_b200 import smoe, synth
+    from paper_2510_05814_b200.multimodel import MultiModel, init_hypotheses
+    cfg = synth.CONFIGS[args.config]
+    C, H, W, K, order = cfg["C"], cfg["H"], cfg["W"], cfg["K"], cfg["order"]
+    target, clean, _ = synth.workload(args.config)
+    pools = init_hypotheses(target, K, args.mm, 1234 + cfg["cfg"] + 1, order)
+    mm = MultiModel(args.mm, K, H, W, C, order)
+    prms = [smoe.Params.from_numpy(p, "cuda") for p in pools]
+    tg = torch.as_tensor(target).cuda()
+    T = args.warmup + args.steps
+    for t in range(args.warmup):
+        mm.step(prms, tg, smoe.LR.paper(t, T))
+    for hd in mm.handles:
+        hd.sync()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for t in range(args.warmup, T):
+        mm.step(prms, tg, smoe.LR.paper(t, T))
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    fused = mm.render(prms).cpu().numpy()
+    psnr = lambda y: float(10 * np.log10(1.0 / np.mean((np.clip(y, 0, 1) - clean) ** 2)))
+    singles = [psnr(mm.handles[i].render(prms[i]).cpu().numpy()) for i in range(args.mm)]
+    out = {"metric": "MM-RSMoE hypothesis iterations/s", "value": args.mm * args.steps / (ms * 1e-3),
+           "unit": "hypothesis-it/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+           "hypotheses": args.mm, "ms_per_step": ms / args.steps, "higher_is_better": True,
+           "config": config_dict(args.config, 1), "data": "synthetic",
+           "psnr_noisy_db": psnr(target), "psnr_single_db_mean": float(np.mean(singles)),
+           "psnr_fused_db": psnr(fused), "l2": "not flushed (concurrent hypotheses)"}
+    print(json.dumps(out))
+    return 0
+
+
 def config_dict(name, world):
     from paper_2510_05814_b200 import synth
     c = synth.CONFIGS[name]
@@ -165,10 +207,14 @@ def main():
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--backward-mode", type=int, default=-1, help="-1 auto (default), 0 pixel-parallel, 1 kernel-parallel")
     ap.add_argument("--no-profile", action="store_true", help="no per-kernel events in the timed region")
+    ap.add_argument("--mm", type=int, default=0,
+                    help="MM-RSMoE (SURVEY f3): fit this many hypotheses concurrently and report the fused denoising")
     args = ap.parse_args()
     assert args.warmup >= 3, "at least 3 warm-up steps"
     if args.impl == "reference":
         return run_reference(args)
+    if args.mm:
+        return run_mm(args)
 
     import numpy as np
     import torch

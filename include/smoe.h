@@ -135,13 +135,17 @@ smoe_status smoe_set_stream(smoe_handle h, void *stream);
  * capacity check) or device (asynchronous). */
 smoe_status smoe_render(smoe_handle h, const smoe_params *p, int out_H, int out_W, float *out);
 
-/* Render options.  sharpen = s in (0, 1]: native sharpening
- * by kernel editing, "reducing the bandwidths of the kernels by a sharpening
- * factor": the render uses Sigma_j -> s Sigma_j (every
- * Cholesky factor times sqrt(s)); s = 1 is the plain render.  The
- * caller's parameters are not modified. */
+/* Render options.  sharpen = s in (0, 1]: native
+ * sharpening by kernel editing, "reducing the bandwidths of the kernels by a
+ * sharpening factor": the render uses Sigma_j -> s Sigma_j
+ * (every Cholesky factor times sqrt(s)); s = 1 is the plain
+ * render.  accumulate = w != 0: out += w y instead of
+ * out = y, so H hypotheses fuse into their average y_m = (1/H) sum_h y_h
+ * (Eq. 11) with w = 1/H; needs a device `out`.  The caller's
+ * parameters are not modified. */
 typedef struct {
     float sharpen;
+    float accumulate;
 } smoe_render_options;
 smoe_status smoe_render_ex(smoe_handle h, const smoe_params *p, int out_H, int out_W, float *out,
                            const smoe_render_options *opt);

@@ -874,6 +874,8 @@ smoe_status smoe_render_ex(smoe_handle h, const smoe_params *p, int out_H, int o
             throw SmoeError(SMOE_ERR_INVALID_ARG, "smoe_render: sharpen must be in (0, 1]");
         float lscale = sqrtf(sharpen);
         bool odev = is_device_ptr(out);
+        if (!odev && opt && opt->accumulate != 0.0f)
+            throw SmoeError(SMOE_ERR_INVALID_ARG, "smoe_render_ex: accumulate needs a device output");
         for (int attempt = 0;; attempt++) {
             Grid &g = h->render;
             ensure_grid(h, g, &h->ctl->render, out_H, out_W);
@@ -886,6 +888,7 @@ smoe_status smoe_render_ex(smoe_handle h, const smoe_params *p, int out_H, int o
             A.nx = g.nx; A.tile0 = 0; A.oW = out_W; A.oH = out_H;
             A.sx = (float)h->W / (float)out_W; A.sy = (float)h->H / (float)out_H;
             A.R2 = h->R2; A.out = o; A.rbf = h->head;
+            A.accum = opt ? opt->accumulate : 0.0f;
             A.work = h->prof.d_work;
             launch(h, SMOE_KERNEL_RASTER_RENDER, "k_raster<render>", [&] {
                 const void *f = nullptr;

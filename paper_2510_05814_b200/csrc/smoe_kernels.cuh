@@ -556,6 +556,7 @@ struct RasterArgs {
     double *dstats;       // SSE, clamped SSE, uncovered pixels
     // render
     float *out;           // [C][oH][oW]
+    float accum;          // 0: out = y; else out += accum * y
     // profiling (PROF instantiation only): tested / hit (pixel, kernel) pairs
     unsigned long long *work;
 };
@@ -725,10 +726,16 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
 
     if (!TRAIN) {
         size_t plane = (size_t)A.oH * A.oW;
+        float *o0 = A.out + (size_t)py0 * A.oW + px, *o1 = A.out + (size_t)py1 * A.oW + px;
 #pragma unroll
         for (int c = 0; c < C; c++) {
-            if (v0) A.out[c * plane + (size_t)py0 * A.oW + px] = y0[c];
-            if (v1) A.out[c * plane + (size_t)py1 * A.oW + px] = y1[c];
+            if (A.accum != 0.f) {          // multi-model fusion: out += w y (Eq. 11)
+                if (v0) o0[c * plane] = fmaf(A.accum, y0[c], o0[c * plane]);
+                if (v1) o1[c * plane] = fmaf(A.accum, y1[c], o1[c * plane]);
+            } else {
+                if (v0) o0[c * plane] = y0[c];
+                if (v1) o1[c * plane] = y1[c];
+            }
         }
         return;
     }

@@ -64,7 +64,7 @@ class c_options(ctypes.Structure):
 
 
 class c_render_options(ctypes.Structure):
-    _fields_ = [("sharpen", ctypes.c_float)]
+    _fields_ = [("sharpen", ctypes.c_float), ("accumulate", ctypes.c_float)]
 
 
 def lib():
@@ -252,15 +252,16 @@ class SMoE:
         return None
 
     def render(self, params: Params, out_H: int | None = None, out_W: int | None = None, out=None,
-               sharpen: float = 1.0):
+               sharpen: float = 1.0, accumulate: float = 0.0):
         """smoe_render(_ex): y on an out_H x out_W raster -> [C, out_H, out_W];
-        ``sharpen`` = s < 1 renders with Sigma -> s Sigma (kernel editing)."""
+        ``sharpen`` = s < 1 renders with Sigma -> s Sigma (kernel editing);
+        ``accumulate`` = w != 0 adds w y into ``out`` (multi-model fusion)."""
         self._stream()
         out_H = self.H if out_H is None else out_H
         out_W = self.W if out_W is None else out_W
         if out is None:
             out = torch.empty((self.C, out_H, out_W), dtype=torch.float32, device=f"cuda:{self.device}")
-        ro = c_render_options(sharpen)
+        ro = c_render_options(sharpen, accumulate)
         _check(lib().smoe_render_ex(self.h, ctypes.byref(params.c()), out_H, out_W, _ptr(out), ctypes.byref(ro)),
                self.h)
         return out

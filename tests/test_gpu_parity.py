@@ -436,3 +436,35 @@ def test_dense_global_model_parity():
     g, _ = h.grad(dev_pool(pool), torch.as_tensor(target).cuda())
     lg = O.loss_grad(opar(pool), target.astype(np.float64), R2=float("inf"))
     assert_grads(g.cpu().numpy(), lg.grad, lg.grad_abs)
+
+
+# ------------------------------------------------------ NEXT row f3 (GPU) --
+
+def test_multimodel_fusion_and_fit():
+    """f3: MM-RSMoE.  The fused render equals the mean of the
+    oracle renders of the H fitted hypotheses (Eq. 11), every hypothesis'
+    fit follows the oracle fit, and fusing reduces the error to the clean
+    image on a noisy input (the denoising effect of Eq. 14)."""
+    from paper_2510_05814_b200.multimodel import MultiModel, init_hypotheses
+    Hh, Ww, C, K, NH, T = 48, 48, 1, 60, 4, 30
+    clean = synth.image(Hh, Ww, C, 301)
+    noisy = synth.noisy(clean, 25 / 255, 302)
+    pools = init_hypotheses(noisy, K, NH, 303)
+    pools = [conditioned(p, Hh, Ww) for p in pools]
+    mm = MultiModel(NH, K, Hh, Ww, C, 0)
+    prms = [dev_pool(p) for p in pools]
+    mm.fit(prms, torch.as_tensor(noisy).cuda(), T)
+    fused = mm.render(prms).cpu().numpy()
+    # fusion is exact: mean of the oracle renders of the GPU-fitted parameters
+    ref = np.mean([O.render(opar(p), Hh, Ww)[0] for p in prms], axis=0)
+    assert_pixels(fused, ref, rel=2e-5, abs_=2e-6)
+    # each hypothesis follows the oracle trajectory (PSNR within 0.01 dB)
+    for p0, pg in zip(pools[:2], prms[:2]):
+        q, _ = O.fit(opar(p0), noisy.astype(np.float64), T)
+        a = O.loss_grad(q, noisy.astype(np.float64)).psnr
+        b = O.loss_grad(opar(pg), noisy.astype(np.float64)).psnr
+        assert abs(a - b) < 0.01
+    # fused prediction is closer to the clean image than a single hypothesis
+    err = lambda y: float(np.mean((np.clip(y, 0, 1) - clean) ** 2))
+    single = [err(O.render(opar(p), Hh, Ww)[0]) for p in prms]
+    assert err(fused) < np.mean(single)
