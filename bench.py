@@ -155,7 +155,17 @@ def run_mm(args):
     cfg = synth.CONFIGS[args.config]
     C, H, W, K, order = cfg["C"], cfg["H"], cfg["W"], cfg["K"], cfg["order"]
     target, clean, _ = synth.workload(args.config)
-    pools = init_hypotheses(target, K, args.mm, 1234 + cfg["cfg"] + 1, order)
+    seg_info = None
+    if args.seg > 0:
+        t0 = time.perf_counter()
+        labels, nseg = smoe.segment(np.clip(target, 0, 1), args.seg, 16)
+        t1 = time.perf_counter()
+        pools = [smoe.segment_init(target, labels, nseg, K, order, seed=1234 + cfg["cfg"] + 1 + h)
+                 for h in range(args.mm)]
+        t2 = time.perf_counter()
+        seg_info = {"threshold": args.seg, "segments": nseg, "segment_s": t1 - t0, "init_s": (t2 - t1) / args.mm}
+    else:
+        pools = init_hypotheses(target, K, args.mm, 1234 + cfg["cfg"] + 1, order)
     mm = MultiModel(args.mm, K, H, W, C, order)
     prms = [smoe.Params.from_numpy(p, "cuda") for p in pools]
     tg = torch.as_tensor(target).cuda()
@@ -180,7 +190,8 @@ def run_mm(args):
            "hypotheses": args.mm, "ms_per_step": ms / args.steps, "higher_is_better": True,
            "config": config_dict(args.config, 1), "data": "synthetic",
            "psnr_noisy_db": psnr(target), "psnr_single_db_mean": float(np.mean(singles)),
-           "psnr_fused_db": psnr(fused), "l2": "not flushed (concurrent hypotheses)"}
+           "psnr_fused_db": psnr(fused), "l2": "not flushed (concurrent hypotheses)",
+           "init": seg_info or "paper random init per hypothesis (seed + shift)"}
     print(json.dumps(out))
     return 0
 
@@ -207,6 +218,8 @@ def main():
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--backward-mode", type=int, default=-1, help="-1 auto (default), 0 pixel-parallel, 1 kernel-parallel")
     ap.add_argument("--no-profile", action="store_true", help="no per-kernel events in the timed region")
+    ap.add_argument("--seg", type=float, default=0.0,
+                    help="with --mm: segmentation-guided init (SURVEY f4) at this threshold (0-255 scale)")
     ap.add_argument("--mm", type=int, default=0,
                     help="MM-RSMoE (SURVEY f3): fit this many hypotheses concurrently and report the fused denoising")
     args = ap.parse_args()

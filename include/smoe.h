@@ -227,6 +227,25 @@ smoe_status smoe_profile_begin(smoe_handle h, int max_launches, unsigned kernel_
 smoe_status smoe_profile_end(smoe_handle h, smoe_kernel_time *times, smoe_work *work);
 const char *smoe_kernel_name(int id);
 
+/* Segmentation-guided initialisation (Eq. 9,
+ * P:424 thresholds 10/20), host code run once before a fit.  The paper only
+ * cites its "modified DBSCAN"; this implements the reading of S:417-438:
+ * smoe_segment: 4-connected region growing on the host image[C][H][W] in
+ * [0,1]: a pixel joins the region when the max-channel |pixel - running
+ * mean| <= threshold (0-255 scale); regions smaller than min_size merge into
+ * the closest adjacent region.  labels[H][W] (host) receive ids 0..N-1,
+ * *n_segments = N.
+ * smoe_segment_init: K kernels over the N segments, max(1, floor(K|R|/HW))
+ * each plus largest-remainder top-up to exactly K (Eq. 9: |B_j| ~ |R_j|/n_k);
+ * centres uniform over the segment's pixels, L = (scale_px, 0, scale_px),
+ * log_pi = 0, expert = segment mean colour, slopes 0.  Outputs are HOST
+ * arrays in the smoe_params layout.  K < N gives SMOE_ERR_INVALID_ARG. */
+smoe_status smoe_segment(const float *image, int H, int W, int C, float threshold, int min_size, int *labels,
+                         int *n_segments);
+smoe_status smoe_segment_init(const float *image, int H, int W, int C, const int *labels, int n_segments, int K,
+                              int expert_order, unsigned long long seed, float scale_px, float *mu, float *chol,
+                              float *log_pi, float *expert);
+
 /* Number of device kernel launches issued by the library since creation. */
 long long smoe_launch_count(smoe_handle h);
 

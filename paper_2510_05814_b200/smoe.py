@@ -104,6 +104,8 @@ def lib():
         "smoe_status_string": (ctypes.c_char_p, [st]),
         "smoe_last_error": (ctypes.c_char_p, [H]),
         "smoe_abi_version": (I, []),
+        "smoe_segment": (st, [P, I, I, I, ctypes.c_float, I, P, ctypes.POINTER(I)]),
+        "smoe_segment_init": (st, [P, I, I, I, P, I, I, I, ctypes.c_ulonglong, ctypes.c_float, P, P, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -374,3 +376,35 @@ def smoe_bin(h: SMoE, params, out_H=None, out_W=None):
 
 def smoe_destroy(h: SMoE):
     h.close()
+
+
+def segment(image, threshold: float = 10.0, min_size: int = 16):
+    """smoe_segment: region labels [H, W] (int32 numpy) and the segment count
+    for a [C, H, W] float32 host image in [0, 1]."""
+    import numpy as np
+    img = np.ascontiguousarray(image, dtype=np.float32)
+    C, H, W = img.shape
+    labels = np.empty((H, W), np.int32)
+    n = ctypes.c_int()
+    _check(lib().smoe_segment(img.ctypes.data, H, W, C, float(threshold), int(min_size), labels.ctypes.data,
+                              ctypes.byref(n)))
+    return labels, n.value
+
+
+def segment_init(image, labels, n_segments: int, K: int, order: int = 0, seed: int = 0, scale_px: float = 5.0):
+    """smoe_segment_init: a kernel pool (numpy, smoe_params layout) spread
+    over the segments by Eq. 9 with the experts at the segment colours."""
+    import numpy as np
+    from .synth import Pool
+    img = np.ascontiguousarray(image, dtype=np.float32)
+    C, H, W = img.shape
+    E = 1 + 2 * order
+    lab = np.ascontiguousarray(labels, dtype=np.int32)
+    mu = np.empty((K, 2), np.float32)
+    chol = np.empty((K, 3), np.float32)
+    lp = np.empty(K, np.float32)
+    ex = np.empty((K, C, E), np.float32)
+    _check(lib().smoe_segment_init(img.ctypes.data, H, W, C, lab.ctypes.data, int(n_segments), int(K), int(order),
+                                   int(seed), float(scale_px), mu.ctypes.data, chol.ctypes.data, lp.ctypes.data,
+                                   ex.ctypes.data))
+    return Pool(mu, chol, lp, ex)
