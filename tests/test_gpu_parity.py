@@ -468,3 +468,70 @@ def test_multimodel_fusion_and_fit():
     err = lambda y: float(np.mean((np.clip(y, 0, 1) - clean) ** 2))
     single = [err(O.render(opar(p), Hh, Ww)[0]) for p in prms]
     assert err(fused) < np.mean(single)
+
+
+# ------------------------------------------------------------- edge cases --
+
+@pytest.mark.parametrize("H,W", [(1, 1), (1, 17), (19, 1), (16, 16), (17, 33)])
+def test_degenerate_image_shapes(H, W):
+    """1-pixel and 1-row/column images, exact and ragged block multiples:
+    render, loss and gradients still match the oracle."""
+    C, K = 3, 5
+    g = np.random.default_rng(H * 100 + W)
+    pool = synth.aniso_pool(H, W, C, K, H + W, order=1, l_range=(1.0, 3.0), shear=0.5)
+    pool.mu[:] = np.stack([g.uniform(-0.5, W - 0.5, K), g.uniform(-0.5, H - 0.5, K)], 1).astype(np.float32)
+    pool = conditioned(pool, H, W)
+    target = synth.image(max(H, 2), max(W, 2), C, 7)[:, :H, :W].copy()
+    h = smoe.SMoE(K, H, W, C, 1)
+    y = h.render(dev_pool(pool)).cpu().numpy()
+    y_ref, _ = O.render(opar(pool), H, W)
+    assert_pixels(y, y_ref)
+    gr, sums = h.grad(dev_pool(pool), torch.as_tensor(target).cuda())
+    lg = O.loss_grad(opar(pool), target.astype(np.float64))
+    assert abs(float(sums[0]) - lg.sse) <= 1e-5 * max(lg.sse, 1e-12)
+    assert_grads(gr.cpu().numpy(), lg.grad, lg.grad_abs)
+
+
+def test_single_kernel_and_image_covering_kernel():
+    """K = 1 (every covered pixel equals the expert) and one kernel whose box
+    covers the whole image next to small ones."""
+    H, W, C = 40, 50, 3
+    pool = synth.aniso_pool(H, W, C, 1, 3)
+    pool.mu[0] = [20.3, 19.6]
+    pool.chol[0] = [6.0, 1.0, 5.0]
+    h = smoe.SMoE(1, H, W, C, 0)
+    y = h.render(dev_pool(pool)).cpu().numpy()
+    y_ref, D = O.render(opar(pool), H, W)
+    assert_pixels(y, y_ref)
+    assert np.allclose(y[:, D > 0], pool.expert[0, :, 0][:, None], atol=1e-6)
+    big = synth.aniso_pool(H, W, C, 30, 4)
+    big.chol[0] = [400.0, 0.0, 400.0]              # covers everything, every block lists it
+    big = conditioned(big, H, W)
+    h2 = smoe.SMoE(30, H, W, C, 0)
+    target = synth.image(H, W, C, 5)
+    gr, _ = h2.grad(dev_pool(big), torch.as_tensor(target).cuda())
+    lg = O.loss_grad(opar(big), target.astype(np.float64))
+    assert lg.uncovered == 0
+    assert_grads(gr.cpu().numpy(), lg.grad, lg.grad_abs)
+
+
+def test_band_with_kernel_parallel_backward_and_graph_replay():
+    """Bands + kernel-parallel backward + repeated graph replays: per-band
+    gradients sum to the full one, and replays are stable."""
+    H, W, C, K = 96, 64, 3, 300
+    pool = conditioned(synth.aniso_pool(H, W, C, K, 44, order=1), H, W)
+    target = torch.as_tensor(synth.image(H, W, C, 45)).cuda()
+    h = smoe.SMoE(K, H, W, C, 1, backward_mode=1)
+    p = dev_pool(pool)
+    full = [h.grad(p, target)[0].clone() for _ in range(3)]     # first eager, then graph replays
+    for f in full[1:]:
+        assert torch.allclose(f, full[0], rtol=1e-5, atol=1e-9)
+    acc = torch.zeros_like(full[0])
+    for r0, r1 in [(0, 1), (1, 4), (4, 6)]:
+        h.set_band(r0, r1)
+        for _ in range(2):
+            g, _ = h.grad(p, target)
+        acc += g
+    h.set_band(0, 0)
+    lg = O.loss_grad(opar(pool), target.cpu().numpy().astype(np.float64))
+    assert_grads(acc.cpu().numpy(), lg.grad, lg.grad_abs, what="band sum (kernel-parallel)")
