@@ -309,6 +309,14 @@ int effective_bwd(smoe_ctx *h)
         else { constexpr int C_ = 3, E_ = 3; BODY; }                          \
     } while (0)
 
+// LPT block order: built by the preprocess's last CTA for grids up to
+// SCAN_SINGLE_MAX blocks (larger grids run several waves where the hardware
+// scheduler balances, and use the look-back scan).
+#ifndef SMOE_LPT
+#define SMOE_LPT 1
+#endif
+bool use_lpt(const Grid &g) { return SMOE_LPT && !g.lb_state && !getenv("SMOE_NO_LPT"); }
+
 ParamsDev pdev(const smoe_params *p) { return ParamsDev{p->mu, p->chol, p->log_pi, p->expert}; }
 
 void check_params(const smoe_params *p)
@@ -332,7 +340,8 @@ void bin(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_hi, bool 
         DISPATCH_CE(h, (k_preprocess<C_, E_><<<nb, PRE_NT, 0, h->stream>>>(
                            K, pdev(p), h->R2, sx, sy, g.oW, g.oH, g.nx, ty_lo, ty_hi, h->rec, h->tbox,
                            g.cnt, &h->ctl->hc, g.n_tiles, g.start, g.cursor, g.cap, g.gc,
-                           zero_stats ? h->ctl->dstats : nullptr, g.lb_state ? nullptr : g.order, lscale)));
+                           zero_stats ? h->ctl->dstats : nullptr, g.lb_state ? nullptr : g.order, lscale,
+                           use_lpt(g) ? 1 : 0)));
     });
     if (g.lb_state) {
         int nb2 = (g.n_tiles + LB_CHUNK - 1) / LB_CHUNK;
@@ -383,7 +392,7 @@ void forward_backward(smoe_ctx *h, const smoe_params *p, const float *target)
     if (nt <= 0) return;
     RasterArgs A{};
     A.rec = h->rec; A.ids = g.ids; A.tmp = g.tmp; A.start = g.start; A.gc = g.gc; A.cap = g.cap;
-    A.order = (getenv("SMOE_NO_LPT") || g.lb_state) ? nullptr : g.order;
+    A.order = use_lpt(g) ? g.order : nullptr;
     A.gcw = g.gc; A.n_work = nt; A.n_sm = h->n_sm;
     A.nx = g.nx; A.tile0 = ty_lo * g.nx; A.oW = h->W; A.oH = h->H;
     A.sx = 1.0f; A.sy = 1.0f; A.R2 = h->R2; A.rbf = h->head;
@@ -884,7 +893,7 @@ smoe_status smoe_render_ex(smoe_handle h, const smoe_params *p, int out_H, int o
             float *o = odev ? out : stage(h->stage_out, h->stage_out_n, n);
             RasterArgs A{};
             A.rec = h->rec; A.ids = g.ids; A.tmp = g.tmp; A.start = g.start; A.gc = g.gc; A.cap = g.cap;
-            A.order = g.lb_state ? nullptr : g.order; A.gcw = g.gc; A.n_work = g.n_tiles; A.n_sm = h->n_sm;
+            A.order = use_lpt(g) ? g.order : nullptr; A.gcw = g.gc; A.n_work = g.n_tiles; A.n_sm = h->n_sm;
             A.nx = g.nx; A.tile0 = 0; A.oW = out_W; A.oH = out_H;
             A.sx = (float)h->W / (float)out_W; A.sy = (float)h->H / (float)out_H;
             A.R2 = h->R2; A.out = o; A.rbf = h->head;

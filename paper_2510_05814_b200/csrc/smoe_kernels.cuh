@@ -23,6 +23,16 @@
 namespace smoe {
 
 constexpr int TILE = 16;                 // 16x16 blocks
+// build-time tuning knobs (A/B builds in scripts/; defaults are the tuned values)
+#ifndef SMOE_KPAR_MINB
+#define SMOE_KPAR_MINB 6                 // kernel-parallel raster, linear experts: min CTAs/SM
+#endif
+#ifndef SMOE_KPAR_MINB_CONST
+#define SMOE_KPAR_MINB_CONST 7           // ... constant experts (fewer live sums, no spills at 7)
+#endif
+#ifndef SMOE_RASTER_BATCH
+#define SMOE_RASTER_BATCH 128            // kernel records staged per shared-memory batch
+#endif
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int SORT_CAP = 2048;           // bucket size sorted in one smem pass
@@ -209,7 +219,7 @@ k_preprocess(int K, ParamsDev p, float R2, float sx /* oW/W */, float sy /* oH/H
              int nx, int ty_lo, int ty_hi, float *__restrict__ rec,
              int4 *__restrict__ tbox, int *__restrict__ cnt, HandleCtr *hc,
              int n_tiles, int *__restrict__ start, int *__restrict__ cursor, long long cap,
-             GridCtr *gc, double *dstats, int *__restrict__ order, float lscale)
+             GridCtr *gc, double *dstats, int *__restrict__ order, float lscale, int build_order)
 {
     int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k < K) preprocess_one<C, E>(k, p, R2, sx, sy, oW, oH, nx, ty_lo, ty_hi, rec, tbox, cnt, hc, lscale);
@@ -225,6 +235,10 @@ k_preprocess(int K, ParamsDev p, float R2, float sx /* oW/W */, float sy /* oH/H
     if (!last) return;
     __threadfence();
     scan_counts<PRE_NT>(cnt, n_tiles, start, cursor, cap, gc, dstats);
+    if (!build_order) {
+        if (threadIdx.x == 0) { gc->ticket = 0; gc->work = 0; }
+        return;
+    }
     // raster work order for the band's blocks: longest lists first (LPT),
     // counting sort on min(|K_n|, 255)
     __shared__ int hist[256];
@@ -611,7 +625,7 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
 {
     using R = Rec<C, E>;
     constexpr int RS4 = R::RS / 4;
-    constexpr int BATCH = 128;
+    constexpr int BATCH = SMOE_RASTER_BATCH;
     constexpr bool MASKS = TRAIN && KPAR;
     __shared__ float4 srec[BATCH * RS4];
     __shared__ int sid[BATCH];
@@ -971,7 +985,7 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
 // SM receives a mix of long and short lists when the whole grid is resident,
 // and later waves start with the longest remaining lists.
 template <int C, int E, bool TRAIN, bool PROF, bool KPAR>
-__global__ void __launch_bounds__(128, KPAR ? 6 : 12)
+__global__ void __launch_bounds__(128, KPAR ? (E == 3 ? SMOE_KPAR_MINB : SMOE_KPAR_MINB_CONST) : 12)
 k_raster(RasterArgs A)
 {
     if (A.gc->pairs > A.cap) return;
