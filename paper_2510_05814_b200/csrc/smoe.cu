@@ -101,6 +101,9 @@ struct Grid {
     int *cnt = nullptr, *start = nullptr, *cursor = nullptr, *order = nullptr;
     int *ids = nullptr, *tmp = nullptr;
     unsigned long long *lb_state = nullptr;   // look-back scan status words
+    int *chunk = nullptr, *hist = nullptr;    // fused binning scratch
+    int bin_grid = 0;                         // cooperative grid of k_bin
+    bool order_valid = false;                 // LPT order written by the last binning
     long long cap = 0;
     bool calibrated = false;
     GridCtr *gc = nullptr;   // points into Ctl
@@ -231,7 +234,7 @@ void dfree(T *&p)
 void free_grid(Grid &g)
 {
     dfree(g.cnt); dfree(g.start); dfree(g.cursor); dfree(g.order); dfree(g.ids); dfree(g.tmp);
-    dfree(g.lb_state);
+    dfree(g.lb_state); dfree(g.chunk); dfree(g.hist);
     g = Grid();
 }
 
@@ -251,6 +254,7 @@ void ensure_grid(smoe_ctx *h, Grid &g, GridCtr *gc, int oH, int oW)
     long long cap = g.cap;
     bool cal = g.calibrated && g.oH == oH && g.oW == oW;
     dfree(g.cnt); dfree(g.start); dfree(g.cursor); dfree(g.order); dfree(g.lb_state);
+    dfree(g.chunk); dfree(g.hist);
     g.oH = oH; g.oW = oW;
     g.nx = (oW + TILE - 1) / TILE;
     g.ny = (oH + TILE - 1) / TILE;
@@ -260,15 +264,14 @@ void ensure_grid(smoe_ctx *h, Grid &g, GridCtr *gc, int oH, int oW)
     CK(cudaMalloc(&g.start, sizeof(int) * (g.n_tiles + 1)));
     CK(cudaMalloc(&g.cursor, sizeof(int) * g.n_tiles));
     CK(cudaMalloc(&g.order, sizeof(int) * g.n_tiles));
-    if (g.n_tiles > SCAN_SINGLE_MAX) {
-        size_t nb = (g.n_tiles + LB_CHUNK - 1) / LB_CHUNK;
-        CK(cudaMalloc(&g.lb_state, sizeof(unsigned long long) * nb));
-        CK(cudaMemsetAsync(g.lb_state, 0, sizeof(unsigned long long) * nb, h->stream));
-    }
+    CK(cudaMalloc(&g.hist, sizeof(int) * 512));
+
     CK(cudaMemsetAsync(g.cnt, 0, sizeof(int) * g.n_tiles, h->stream));
     CK(cudaMemsetAsync(gc, 0, sizeof(GridCtr), h->stream));
     g.cap = cap;
     g.calibrated = cal;
+    g.bin_grid = 0;
+    dfree(g.chunk);
 }
 
 void grow(smoe_ctx *h, Grid &g, long long need)
@@ -315,7 +318,7 @@ int effective_bwd(smoe_ctx *h)
 #ifndef SMOE_LPT
 #define SMOE_LPT 1
 #endif
-bool use_lpt(const Grid &g) { return SMOE_LPT && !g.lb_state && !getenv("SMOE_NO_LPT"); }
+bool use_lpt(const Grid &g) { return SMOE_LPT && !g.lb_state && g.n_tiles <= SCAN_SINGLE_MAX && !getenv("SMOE_NO_LPT"); }
 
 ParamsDev pdev(const smoe_params *p) { return ParamsDev{p->mu, p->chol, p->log_pi, p->expert}; }
 
@@ -331,11 +334,16 @@ void check_params(const smoe_params *p)
 // a1-a4: preprocess, scan, scatter, in-bucket sort on grid g for block rows
 // [ty_lo, ty_hi).  The first binning of a grid calibrates the capacity with
 // one synchronous read of P; later binnings never synchronise.
-void bin(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_hi, bool zero_stats, float lscale = 1.0f)
+void bin_unfused(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_hi, bool zero_stats, float lscale)
 {
     int K = h->K;
     int nb = (K + PRE_NT - 1) / PRE_NT;
     float sx = (float)g.oW / (float)h->W, sy = (float)g.oH / (float)h->H;
+    if (g.n_tiles > SCAN_SINGLE_MAX && !g.lb_state) {
+        size_t nbl = (g.n_tiles + LB_CHUNK - 1) / LB_CHUNK;
+        CK(cudaMalloc(&g.lb_state, sizeof(unsigned long long) * nbl));
+        CK(cudaMemsetAsync(g.lb_state, 0, sizeof(unsigned long long) * nbl, h->stream));
+    }
     launch(h, SMOE_KERNEL_PREPROCESS, "k_preprocess", [&] {
         DISPATCH_CE(h, (k_preprocess<C_, E_><<<nb, PRE_NT, 0, h->stream>>>(
                            K, pdev(p), h->R2, sx, sy, g.oW, g.oH, g.nx, ty_lo, ty_hi, h->rec, h->tbox,
@@ -361,6 +369,64 @@ void bin(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_hi, bool 
     launch(h, SMOE_KERNEL_SCATTER, "k_scatter", [&] {
         k_scatter<<<ns, 64, 0, h->stream>>>(K, h->tbox, g.nx, ty_lo, ty_hi, g.cursor, g.ids, g.cap, g.gc);
     });
+    g.order_valid = use_lpt(g);
+}
+
+// a1-a4 binning of grid g for block rows [ty_lo, ty_hi): one cooperative
+// k_bin launch, or k_preprocess (+ k_scan_lookback) + k_scatter.  The
+// cooperative launch costs a few us more than a plain one (measured), so the
+// fused form is used for large pools (K >= 50000: config 3 gains 3%);
+// SMOE_FUSED_BIN=0/1 forces either.  The first binning of a grid calibrates
+// the capacity with one synchronous read of P; later binnings never sync.
+void bin(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_hi, bool zero_stats, float lscale = 1.0f)
+{
+    const char *fe = getenv("SMOE_FUSED_BIN");
+    bool fused = fe ? atoi(fe) != 0 : h->K >= 50000;
+    if (!fused) return bin_unfused(h, g, p, ty_lo, ty_hi, zero_stats, lscale);
+    int K = h->K;
+    if (!g.bin_grid) {
+        int occ = 0;
+        const void *f = nullptr;
+        DISPATCH_CE(h, (f = (const void *)k_bin<C_, E_>));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, BIN_NT, 0));
+        int want = std::max((K + BIN_NT - 1) / BIN_NT, (g.n_tiles + BIN_NT - 1) / BIN_NT);
+        g.bin_grid = std::max(1, std::min(want, std::max(1, occ) * h->n_sm));
+        CK(cudaMalloc(&g.chunk, sizeof(int) * g.bin_grid));
+    }
+    BinArgs B{};
+    B.K = K; B.p = pdev(p); B.R2 = h->R2;
+    B.sx = (float)g.oW / (float)h->W; B.sy = (float)g.oH / (float)h->H; B.lscale = lscale;
+    B.oW = g.oW; B.oH = g.oH; B.nx = g.nx; B.ty_lo = ty_lo; B.ty_hi = ty_hi; B.n_tiles = g.n_tiles;
+    B.rec = h->rec; B.tbox = h->tbox; B.cnt = g.cnt; B.start = g.start; B.cursor = g.cursor; B.ids = g.ids;
+    B.order = SMOE_LPT && !getenv("SMOE_NO_LPT") ? g.order : nullptr;
+    B.chunk = g.chunk; B.hist = g.hist; B.cap = g.cap; B.gc = g.gc; B.hc = &h->ctl->hc;
+    B.dstats = zero_stats ? h->ctl->dstats : nullptr;
+    launch(h, SMOE_KERNEL_PREPROCESS, "k_bin", [&] {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(g.bin_grid);
+        cfg.blockDim = dim3(BIN_NT);
+        cfg.stream = h->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        DISPATCH_CE(h, ((void)cudaLaunchKernelEx(&cfg, k_bin<C_, E_>, B)));
+    });
+    g.order_valid = B.order != nullptr;
+    if (!g.calibrated) {
+        // the scatter phase skipped (capacity 0): size the lists, then scatter
+        long long P;
+        CK(cudaMemcpyAsync(&P, &g.gc->pairs, sizeof(P), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        if (&g == &h->train) h->last_pairs = (double)P;
+        grow(h, g, P > h->init_cap ? P : h->init_cap);
+        int ns = (K + 63) / 64;
+        launch(h, SMOE_KERNEL_SCATTER, "k_scatter", [&] {
+            k_scatter<<<ns, 64, 0, h->stream>>>(K, h->tbox, g.nx, ty_lo, ty_hi, g.cursor, g.ids, g.cap, g.gc);
+        });
+        g.order_valid = false;
+    }
 }
 
 void band_rows(smoe_ctx *h, int &ty_lo, int &ty_hi)
@@ -392,7 +458,7 @@ void forward_backward(smoe_ctx *h, const smoe_params *p, const float *target)
     if (nt <= 0) return;
     RasterArgs A{};
     A.rec = h->rec; A.ids = g.ids; A.tmp = g.tmp; A.start = g.start; A.gc = g.gc; A.cap = g.cap;
-    A.order = use_lpt(g) ? g.order : nullptr;
+    A.order = g.order_valid ? g.order : nullptr;
     A.gcw = g.gc; A.n_work = nt; A.n_sm = h->n_sm;
     A.nx = g.nx; A.tile0 = ty_lo * g.nx; A.oW = h->W; A.oH = h->H;
     A.sx = 1.0f; A.sy = 1.0f; A.R2 = h->R2; A.rbf = h->head;
@@ -893,7 +959,7 @@ smoe_status smoe_render_ex(smoe_handle h, const smoe_params *p, int out_H, int o
             float *o = odev ? out : stage(h->stage_out, h->stage_out_n, n);
             RasterArgs A{};
             A.rec = h->rec; A.ids = g.ids; A.tmp = g.tmp; A.start = g.start; A.gc = g.gc; A.cap = g.cap;
-            A.order = use_lpt(g) ? g.order : nullptr; A.gcw = g.gc; A.n_work = g.n_tiles; A.n_sm = h->n_sm;
+            A.order = g.order_valid ? g.order : nullptr; A.gcw = g.gc; A.n_work = g.n_tiles; A.n_sm = h->n_sm;
             A.nx = g.nx; A.tile0 = 0; A.oW = out_W; A.oH = out_H;
             A.sx = (float)h->W / (float)out_W; A.sy = (float)h->H / (float)out_H;
             A.R2 = h->R2; A.out = o; A.rbf = h->head;

@@ -17,6 +17,7 @@
 // result is the canonical list K_n (Eq. 5): blocks ascending, kernel ids
 // ascending inside a block (Q18).
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -408,6 +409,170 @@ k_scatter(int K, const int4 *__restrict__ tbox, int nx, int ty_lo, int ty_hi,
         for (int q = 0; q < 8; q++)
             if (pos[q] >= 0) ids[pos[q]] = k;
     }
+}
+
+// ------------------------------------------------- a1-a4 fused (default) --
+// One cooperative launch bins a grid: phase 1 preprocesses the kernels and
+// counts (grid-stride, = k_preprocess); phase 2 scans the block counts in
+// parallel (every CTA owns a contiguous chunk of blocks: chunk totals, grid
+// sync, chunk offsets by a CTA-level sum, local scan) and histograms the
+// list lengths for the LPT order; phase 3 scatters the kernel ids into their
+// buckets (= k_scatter) and writes the LPT block order.  Three grid-wide
+// barriers replace two kernel boundaries and the serial last-CTA scan.
+struct BinArgs {
+    int K;
+    ParamsDev p;
+    float R2, sx, sy, lscale;
+    int oW, oH, nx, ty_lo, ty_hi, n_tiles;
+    float *rec;
+    int4 *tbox;
+    int *cnt, *start, *cursor, *ids, *order;
+    int *chunk;          // [gridDim] chunk totals
+    int *hist;           // [512]: LPT bin counts | bin cursors
+    long long cap;
+    GridCtr *gc;
+    HandleCtr *hc;
+    double *dstats;
+};
+
+constexpr int BIN_NT = 256;
+
+template <int C, int E>
+__global__ void __launch_bounds__(BIN_NT)
+k_bin(BinArgs B)
+{
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int nthreads = gridDim.x * BIN_NT;
+    __shared__ int sw[BIN_NT / 32];
+    __shared__ long long s_off;
+    __shared__ int shist[256];
+    // ---- phase 1 (a1) ----
+    if (blockIdx.x == 0) {
+        for (int i = tid; i < 512; i += BIN_NT) B.hist[i] = 0;
+        if (tid < 4 && B.dstats) B.dstats[tid] = 0.0;
+    }
+    for (int k = blockIdx.x * BIN_NT + tid; k < B.K; k += nthreads)
+        preprocess_one<C, E>(k, B.p, B.R2, B.sx, B.sy, B.oW, B.oH, B.nx, B.ty_lo, B.ty_hi, B.rec, B.tbox,
+                             B.cnt, B.hc, B.lscale);
+    grid.sync();
+    // ---- phase 2 (a2): chunked scan of the block counts ----
+    const int n = B.n_tiles;
+    const int ch = (n + gridDim.x - 1) / gridDim.x;
+    const int c0 = min(n, blockIdx.x * ch), c1 = min(n, c0 + ch);
+    int part = 0;
+    for (int i = c0 + tid; i < c1; i += BIN_NT) part += __ldcg(B.cnt + i);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) part += __shfl_xor_sync(FULL, part, o);
+    if (lane == 0) sw[wid] = part;
+    __syncthreads();
+    if (tid == 0) {
+        int t = 0;
+        for (int w = 0; w < BIN_NT / 32; w++) t += sw[w];
+        B.chunk[blockIdx.x] = t;
+    }
+    shist[tid] = 0;
+    grid.sync();
+    {
+        long long off = 0;
+        for (int b = tid; b < (int)blockIdx.x; b += BIN_NT) off += __ldcg(B.chunk + b);
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) off += __shfl_xor_sync(FULL, off, o);
+        __syncthreads();
+        if (lane == 0) sw[wid] = (int)off;
+        __syncthreads();
+        if (tid == 0) {
+            long long t = 0;
+            for (int w = 0; w < BIN_NT / 32; w++) t += sw[w];
+            s_off = t;
+        }
+        __syncthreads();
+    }
+    const int t0 = B.ty_lo * B.nx, t1 = B.ty_hi * B.nx;
+    long long carry = s_off;
+    for (int base = c0; base < c1; base += BIN_NT) {
+        const int i = base + tid;
+        const int v = i < c1 ? __ldcg(B.cnt + i) : 0;
+        int inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(FULL, inc, o);
+            if (lane >= o) inc += t;
+        }
+        __syncthreads();
+        if (lane == 31) sw[wid] = inc;
+        __syncthreads();
+        int wpre = 0, tot = 0;
+#pragma unroll
+        for (int w = 0; w < BIN_NT / 32; w++) {
+            wpre += (w < wid) ? sw[w] : 0;
+            tot += sw[w];
+        }
+        if (i < c1) {
+            const int ex = (int)carry + wpre + inc - v;
+            B.start[i] = ex;
+            B.cursor[i] = ex;
+            B.cnt[i] = 0;
+            if (B.order && i >= t0 && i < t1) atomicAdd(&shist[255 - min(v, 255)], 1);
+        }
+        carry += tot;
+    }
+    __syncthreads();
+    if (B.order && shist[tid]) atomicAdd(&B.hist[tid], shist[tid]);
+    if (blockIdx.x == gridDim.x - 1 && tid == 0) {
+        const long long P = carry;
+        B.start[n] = (int)P;
+        B.gc->pairs = P;
+        if (P > B.cap) {
+            if (P > B.gc->need) B.gc->need = P;
+            B.gc->skipped += 1;
+        }
+    }
+    grid.sync();
+    // ---- phase 3 (a3 + LPT order) ----
+    const long long P = __ldcg(&B.gc->pairs);
+    if (P > B.cap) return;                  // uniform: every CTA reads the same P
+    for (int k = blockIdx.x * BIN_NT + tid; k < B.K; k += nthreads) {
+        int4 tb = B.tbox[k];
+        if (tb.x < 0) continue;
+        int y0 = max(tb.z, B.ty_lo), y1 = min(tb.w, B.ty_hi - 1);
+        if (y0 > y1) continue;
+        const int w = tb.y - tb.x + 1, cnt = w * (y1 - y0 + 1);
+        for (int i0 = 0; i0 < cnt; i0 += 8) {
+            int pos[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                int i = i0 + q;
+                pos[q] = -1;
+                if (i < cnt) pos[q] = atomicAdd(&B.cursor[(y0 + i / w) * B.nx + tb.x + i % w], 1);
+            }
+#pragma unroll
+            for (int q = 0; q < 8; q++)
+                if (pos[q] >= 0) B.ids[pos[q]] = k;
+        }
+    }
+    if (B.order) {
+        // bin bases: exclusive scan of the 256 LPT bins (redundantly per CTA)
+        int v = __ldcg(B.hist + tid), inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(FULL, inc, o);
+            if (lane >= o) inc += t;
+        }
+        if (lane == 31) sw[wid] = inc;
+        __syncthreads();
+        int wpre = 0;
+        for (int w = 0; w < wid; w++) wpre += sw[w];
+        shist[tid] = wpre + inc - v;
+        __syncthreads();
+        for (int i = max(c0, t0) + tid; i < min(c1, t1); i += BIN_NT) {
+            const int c = __ldcg(B.start + i + 1) - __ldcg(B.start + i);
+            const int bin = 255 - min(c, 255);
+            B.order[shist[bin] + atomicAdd(&B.hist[256 + bin], 1)] = i;
+        }
+    }
+    if (blockIdx.x == 0 && tid == 0) { B.gc->ticket = 0; B.gc->work = 0; }
 }
 
 // ---------------------------------------------------------------- a4 ------

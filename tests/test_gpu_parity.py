@@ -53,6 +53,29 @@ def test_binning_bit_exact(H, W, C, K, order, scale, seed):
     np.testing.assert_array_equal(ids.numpy(), ids_ref)
 
 
+@pytest.mark.parametrize("fused", ["0", "1"])
+def test_binning_both_binners(fused, monkeypatch):
+    """The cooperative fused binner (k_bin) and the three-kernel one produce
+    the same canonical lists, with and without a band."""
+    monkeypatch.setenv("SMOE_FUSED_BIN", fused)
+    H, W, C, K = 130, 97, 3, 600
+    pool = conditioned(synth.aniso_pool(H, W, C, K, 5, order=1, margin_px=8), H, W)
+    h = smoe.SMoE(K, H, W, C, 1)
+    rng, ids, tb = h.bin(dev_pool(pool))
+    _, tb_ref, _ = O.boxes(opar(pool), H, W)
+    rng_ref, ids_ref = O.tile_list(tb_ref, 7, 9)
+    np.testing.assert_array_equal(rng.numpy(), rng_ref)
+    np.testing.assert_array_equal(ids.numpy(), ids_ref)
+    target = torch.as_tensor(synth.image(H, W, C, 6)).cuda()
+    lg = O.loss_grad(opar(pool), target.cpu().numpy().astype(np.float64))
+    acc = None
+    for r0, r1 in [(0, 4), (4, 9)]:
+        h.set_band(r0, r1)
+        g, _ = h.grad(dev_pool(pool), target)
+        acc = g if acc is None else acc + g
+    assert_grads(acc.cpu().numpy(), lg.grad, lg.grad_abs)
+
+
 def test_binning_kodak_density_and_determinism():
     """768x512 Kodak-shaped, 10k paper-init kernels (config 2 geometry)."""
     H, W = 512, 768
