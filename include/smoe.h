@@ -179,6 +179,18 @@ smoe_status smoe_apply(smoe_handle h, smoe_params *p, const float *grad, const s
 /* Zero the Adam moments and the step counter. */
 smoe_status smoe_reset_adam(smoe_handle h);
 
+/* Stream-ordered statistics for pipelined loops: smoe_stats_async enqueues
+ * a device->host copy of the most recent step's raw statistics into `dst`
+ * (caller-owned, ideally pinned host memory) without synchronising; once the
+ * caller knows the copy completed (a later smoe_sync, an event, or reading
+ * it k steps later after a sync), smoe_stats_from_raw converts it. */
+typedef struct {
+    double sse, sse_clamped, uncovered;
+    long long pairs;
+} smoe_raw_stats;
+smoe_status smoe_stats_async(smoe_handle h, smoe_raw_stats *dst);
+smoe_status smoe_stats_from_raw(smoe_handle h, const smoe_raw_stats *raw, smoe_stats *out);
+
 /* Wait for the handle's stream and report latched device faults.  If `last`
  * is non-NULL it receives the statistics of the most recent step/grad. */
 smoe_status smoe_sync(smoe_handle h, smoe_stats *last);

@@ -137,7 +137,16 @@ struct smoe_ctx {
     cudaStream_t cap_stream = nullptr;
     std::vector<cudaEvent_t> cap_ev;   // placeholders recorded during capture
     std::vector<int> cap_kid;
-    StepGraph sg_step, sg_grad;
+    StepGraph sg[2][4];         // graph cache per mode (step, grad), LRU by use stamp
+    long long sg_use[2][4] = {{0}};
+    long long sg_clock = 0;
+    // host targets: double-buffered staging on a copy stream, so the H2D copy
+    // of call t+1 overlaps the compute of call t
+    cudaStream_t copy_stream = nullptr;
+    float *tstage[2] = {nullptr, nullptr};
+    cudaEvent_t tcopied[2] = {nullptr, nullptr}, tconsumed[2] = {nullptr, nullptr};
+    int tslot = 0;
+    int tpending = -1;          // slot whose consumption event must follow the current sequence
     Prof prof;
     std::string err;
 };
@@ -440,9 +449,32 @@ const float *stage_target(smoe_ctx *h, const float *target)
 {
     if (is_device_ptr(target)) return target;
     size_t n = (size_t)h->C * h->H * h->W;
-    float *d = stage(h->stage_in, h->stage_in_n, n);
-    CK(cudaMemcpyAsync(d, target, n * sizeof(float), cudaMemcpyHostToDevice, h->stream));
-    return d;
+    if (!h->copy_stream) {
+        CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; i++) {
+            CK(cudaMalloc(&h->tstage[i], n * sizeof(float)));
+            CK(cudaEventCreateWithFlags(&h->tcopied[i], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&h->tconsumed[i], cudaEventDisableTiming));
+            CK(cudaEventRecord(h->tconsumed[i], h->stream));
+        }
+    }
+    const int s = h->tslot;
+    h->tslot ^= 1;
+    CK(cudaStreamWaitEvent(h->copy_stream, h->tconsumed[s], 0));      // buffer no longer read
+    CK(cudaMemcpyAsync(h->tstage[s], target, n * sizeof(float), cudaMemcpyHostToDevice, h->copy_stream));
+    CK(cudaEventRecord(h->tcopied[s], h->copy_stream));
+    CK(cudaStreamWaitEvent(h->stream, h->tcopied[s], 0));
+    h->tpending = s;
+    return h->tstage[s];
+}
+
+// After the launch sequence that read a staged target: mark its buffer free.
+void release_target(smoe_ctx *h)
+{
+    if (h->tpending >= 0) {
+        CK(cudaEventRecord(h->tconsumed[h->tpending], h->stream));
+        h->tpending = -1;
+    }
 }
 
 // a1-a7 on the training grid (current band): raw sums into h->acc, loss
@@ -667,16 +699,27 @@ void replay(smoe_ctx *h, StepGraph &g, const smoe_params *p, float *gout, const 
 // is calibrated, eager launches otherwise.
 void run_sequence(smoe_ctx *h, int mode, const smoe_params *p, const float *t, float *gout, const smoe_lr *lr)
 {
-    StepGraph &g = mode == 0 ? h->sg_step : h->sg_grad;
     bool ready = h->use_graphs && h->train.calibrated && h->train.oH == h->H && h->train.oW == h->W &&
                  h->train.cnt != nullptr;
     if (!ready) {
         forward_backward(h, p, t);
         launch_adam(h, mode, p, nullptr, gout, lr);
+        release_target(h);
         return;
     }
-    if (!graph_matches(h, g, p, t, gout)) capture(h, g, mode, p, t, gout, lr);
-    replay(h, g, p, gout, lr);
+    // graph cache lookup (key: buffers, band, modes); evict the least recent
+    int hit = -1, lru = 0;
+    for (int i = 0; i < 4; i++) {
+        if (graph_matches(h, h->sg[mode][i], p, t, gout)) hit = i;
+        if (h->sg_use[mode][i] < h->sg_use[mode][lru]) lru = i;
+    }
+    if (hit < 0) {
+        hit = lru;
+        capture(h, h->sg[mode][hit], mode, p, t, gout, lr);
+    }
+    h->sg_use[mode][hit] = ++h->sg_clock;
+    replay(h, h->sg[mode][hit], p, gout, lr);
+    release_target(h);
 }
 
 }  // namespace
@@ -809,8 +852,14 @@ smoe_status smoe_destroy(smoe_handle h)
     if (h->h_ctl) cudaFreeHost(h->h_ctl);
     for (cudaEvent_t e : h->prof.ev) cudaEventDestroy(e);
     for (cudaEvent_t e : h->cap_ev) cudaEventDestroy(e);
-    destroy_graph(h->sg_step);
-    destroy_graph(h->sg_grad);
+    for (int m = 0; m < 2; m++)
+        for (int i = 0; i < 4; i++) destroy_graph(h->sg[m][i]);
+    if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+    for (int i = 0; i < 2; i++) {
+        dfree(h->tstage[i]);
+        if (h->tcopied[i]) cudaEventDestroy(h->tcopied[i]);
+        if (h->tconsumed[i]) cudaEventDestroy(h->tconsumed[i]);
+    }
     if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
     dfree(h->prof.d_work);
     (void)cudaGetLastError();
@@ -1020,6 +1069,33 @@ smoe_status smoe_bin(smoe_handle h, const smoe_params *p, int out_H, int out_W, 
 }
 
 long long smoe_launch_count(smoe_handle h) { return h ? h->launches : -1; }
+
+smoe_status smoe_stats_async(smoe_handle h, smoe_raw_stats *dst)
+{
+    if (!h) return SMOE_ERR_BAD_HANDLE;
+    if (!dst) { set_err(h, "smoe_stats_async: NULL dst"); return SMOE_ERR_INVALID_ARG; }
+    return guard(h, [&]() {
+        CK(cudaMemcpyAsync(&dst->sse, h->ctl->dstats, 3 * sizeof(double), cudaMemcpyDefault, h->stream));
+        CK(cudaMemcpyAsync(&dst->pairs, &h->ctl->train.pairs, sizeof(long long), cudaMemcpyDefault, h->stream));
+        return SMOE_OK;
+    });
+}
+
+smoe_status smoe_stats_from_raw(smoe_handle h, const smoe_raw_stats *raw, smoe_stats *out)
+{
+    if (!h) return SMOE_ERR_BAD_HANDLE;
+    if (!raw || !out) return SMOE_ERR_INVALID_ARG;
+    double n = (double)h->H * h->W * h->C;
+    out->sse = raw->sse;
+    out->sse_clamped = raw->sse_clamped;
+    out->uncovered_px = (long long)raw->uncovered;
+    out->loss = raw->sse / n;
+    double mse_c = raw->sse_clamped / n;
+    out->psnr_db = mse_c > 0 ? 10.0 * std::log10(1.0 / mse_c) : INFINITY;
+    out->pairs = raw->pairs;
+    out->n_tiles = h->train.n_tiles;
+    return SMOE_OK;
+}
 
 const char *smoe_kernel_name(int id)
 {

@@ -56,6 +56,11 @@ class c_work(ctypes.Structure):
 KERNEL_COUNT = 5
 
 
+class c_raw_stats(ctypes.Structure):
+    _fields_ = [("sse", ctypes.c_double), ("sse_clamped", ctypes.c_double), ("uncovered", ctypes.c_double),
+                ("pairs", ctypes.c_longlong)]
+
+
 class c_options(ctypes.Structure):
     _fields_ = [("K", ctypes.c_int), ("H", ctypes.c_int), ("W", ctypes.c_int), ("C", ctypes.c_int),
                 ("expert_order", ctypes.c_int), ("R2", ctypes.c_double), ("device", ctypes.c_int),
@@ -104,6 +109,8 @@ def lib():
         "smoe_status_string": (ctypes.c_char_p, [st]),
         "smoe_last_error": (ctypes.c_char_p, [H]),
         "smoe_abi_version": (I, []),
+        "smoe_stats_async": (st, [H, P]),
+        "smoe_stats_from_raw": (st, [H, P, ctypes.POINTER(c_stats)]),
         "smoe_segment": (st, [P, I, I, I, ctypes.c_float, I, P, ctypes.POINTER(I)]),
         "smoe_segment_init": (st, [P, I, I, I, P, I, I, I, ctypes.c_ulonglong, ctypes.c_float, P, P, P, P]),
     }
@@ -289,6 +296,17 @@ class SMoE:
 
     def reset_adam(self):
         _check(lib().smoe_reset_adam(self.h), self.h)
+
+    def stats_async(self, dst_ptr: int):
+        """smoe_stats_async: enqueue the D2H copy of the last step's raw
+        statistics into host memory at dst_ptr (a c_raw_stats, ideally pinned)."""
+        self._stream()
+        _check(lib().smoe_stats_async(self.h, ctypes.c_void_p(dst_ptr)), self.h)
+
+    def stats_from_raw(self, src_ptr: int) -> Stats:
+        s = c_stats()
+        _check(lib().smoe_stats_from_raw(self.h, ctypes.c_void_p(src_ptr), ctypes.byref(s)), self.h)
+        return Stats.of(s)
 
     def sync(self) -> Stats:
         s = c_stats()
