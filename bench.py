@@ -366,7 +366,18 @@ def main():
                 torch.cuda.synchronize()
                 rt += e0.elapsed_time(e1)
             h.sync()
-            render[f"x{s}"] = {"mpix_s": oH * oW * reps / (rt * 1e-3) / 1e6, "ms": rt / reps, "out": [oH, oW]}
+            # work counts of one render (device counters) for its roofline
+            h.profile_begin(4, kernels=["k_raster<render>"], count_work=True)
+            h.render(params, oH, oW, out)
+            rk, (r_tested, r_hit) = h.profile_end()
+            a_f = 2 + C + 2 * C * order
+            peak = 148 * 128 * load_peaks()[0].get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+            rast_ms = rk.get("k_raster<render>", (rt / reps, 1))
+            ach = (7 * r_tested + a_f * r_hit) / (rast_ms[0] / rast_ms[1] * 1e-3) / 1e12
+            render[f"x{s}"] = {"mpix_s": oH * oW * reps / (rt * 1e-3) / 1e6, "ms": rt / reps, "out": [oH, oW],
+                               "raster_roofline": {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                                                   "frac": ach / peak, "tested_pairs": r_tested, "hit_pairs": r_hit,
+                                                   "ops_note": f"7/tested + {a_f}/hit FP32 lane-ops"}}
 
     # e2e through the public API: every step copies its target from pinned
     # host memory (the library double-buffers it on a copy stream, so the
