@@ -179,6 +179,14 @@ smoe_status smoe_apply(smoe_handle h, smoe_params *p, const float *grad, const s
 /* Zero the Adam moments and the step counter. */
 smoe_status smoe_reset_adam(smoe_handle h);
 
+/* Checkpoint / resume of the optimiser state: the first and
+ * second Adam moments as m1[K][Pk], m2[K][Pk] float32 (gradient layout, host
+ * or device) and the step counter t.  Together with the caller-owned
+ * parameters this resumes a fit (identical up to the run-to-run rounding
+ * order of the backward's float atomics).  Synchronous. */
+smoe_status smoe_get_adam(smoe_handle h, float *m1, float *m2, long long *t);
+smoe_status smoe_set_adam(smoe_handle h, const float *m1, const float *m2, long long t);
+
 /* Stream-ordered statistics for pipelined loops: smoe_stats_async enqueues
  * a device->host copy of the most recent step's raw statistics into `dst`
  * (caller-owned, ideally pinned host memory) without synchronising; once the

@@ -1070,6 +1070,56 @@ smoe_status smoe_bin(smoe_handle h, const smoe_params *p, int out_H, int out_W, 
 
 long long smoe_launch_count(smoe_handle h) { return h ? h->launches : -1; }
 
+smoe_status smoe_get_adam(smoe_handle h, float *m1, float *m2, long long *t)
+{
+    if (!h) return SMOE_ERR_BAD_HANDLE;
+    if (!m1 || !m2 || !t) { set_err(h, "smoe_get_adam: NULL argument"); return SMOE_ERR_INVALID_ARG; }
+    return guard(h, [&]() {
+        size_t n = (size_t)h->K * h->P;
+        CK(cudaStreamSynchronize(h->stream));
+        // library layout is parameter-major [Pk][K]; the ABI layout is [K][Pk]
+        std::vector<float> a(n), b(n);
+        CK(cudaMemcpy(a.data(), h->m1, n * sizeof(float), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(b.data(), h->m2, n * sizeof(float), cudaMemcpyDeviceToHost));
+        std::vector<float> ta(n), tb(n);
+        for (int i = 0; i < h->P; i++)
+            for (int k = 0; k < h->K; k++) {
+                ta[(size_t)k * h->P + i] = a[(size_t)i * h->K + k];
+                tb[(size_t)k * h->P + i] = b[(size_t)i * h->K + k];
+            }
+        CK(cudaMemcpy(m1, ta.data(), n * sizeof(float), cudaMemcpyDefault));
+        CK(cudaMemcpy(m2, tb.data(), n * sizeof(float), cudaMemcpyDefault));
+        HandleCtr hc;
+        CK(cudaMemcpy(&hc, &h->ctl->hc, sizeof(hc), cudaMemcpyDeviceToHost));
+        *t = hc.t;
+        return SMOE_OK;
+    });
+}
+
+smoe_status smoe_set_adam(smoe_handle h, const float *m1, const float *m2, long long t)
+{
+    if (!h) return SMOE_ERR_BAD_HANDLE;
+    if (!m1 || !m2 || t < 0) { set_err(h, "smoe_set_adam: bad argument"); return SMOE_ERR_INVALID_ARG; }
+    return guard(h, [&]() {
+        size_t n = (size_t)h->K * h->P;
+        std::vector<float> a(n), b(n), ta(n), tb(n);
+        CK(cudaMemcpy(a.data(), m1, n * sizeof(float), cudaMemcpyDefault));
+        CK(cudaMemcpy(b.data(), m2, n * sizeof(float), cudaMemcpyDefault));
+        for (int i = 0; i < h->P; i++)
+            for (int k = 0; k < h->K; k++) {
+                ta[(size_t)i * h->K + k] = a[(size_t)k * h->P + i];
+                tb[(size_t)i * h->K + k] = b[(size_t)k * h->P + i];
+            }
+        CK(cudaStreamSynchronize(h->stream));
+        CK(cudaMemcpy(h->m1, ta.data(), n * sizeof(float), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->m2, tb.data(), n * sizeof(float), cudaMemcpyHostToDevice));
+        HandleCtr hc{};
+        hc.t = t;
+        CK(cudaMemcpy(&h->ctl->hc, &hc, sizeof(hc), cudaMemcpyHostToDevice));
+        return SMOE_OK;
+    });
+}
+
 smoe_status smoe_stats_async(smoe_handle h, smoe_raw_stats *dst)
 {
     if (!h) return SMOE_ERR_BAD_HANDLE;

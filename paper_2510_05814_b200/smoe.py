@@ -110,6 +110,8 @@ def lib():
         "smoe_last_error": (ctypes.c_char_p, [H]),
         "smoe_abi_version": (I, []),
         "smoe_stats_async": (st, [H, P]),
+        "smoe_get_adam": (st, [H, P, P, ctypes.POINTER(ctypes.c_longlong)]),
+        "smoe_set_adam": (st, [H, P, P, ctypes.c_longlong]),
         "smoe_stats_from_raw": (st, [H, P, ctypes.POINTER(c_stats)]),
         "smoe_segment": (st, [P, I, I, I, ctypes.c_float, I, P, ctypes.POINTER(I)]),
         "smoe_segment_init": (st, [P, I, I, I, P, I, I, I, ctypes.c_ulonglong, ctypes.c_float, P, P, P, P]),
@@ -296,6 +298,20 @@ class SMoE:
 
     def reset_adam(self):
         _check(lib().smoe_reset_adam(self.h), self.h)
+
+    def get_adam(self):
+        """smoe_get_adam -> (m1[K,Pk], m2[K,Pk], t): optimiser checkpoint."""
+        m1 = torch.empty((self.K, self.Pk), dtype=torch.float32)
+        m2 = torch.empty((self.K, self.Pk), dtype=torch.float32)
+        t = ctypes.c_longlong()
+        _check(lib().smoe_get_adam(self.h, m1.data_ptr(), m2.data_ptr(), ctypes.byref(t)), self.h)
+        return m1, m2, t.value
+
+    def set_adam(self, m1, m2, t: int):
+        """smoe_set_adam: restore an optimiser checkpoint."""
+        m1 = m1.contiguous().float()
+        m2 = m2.contiguous().float()
+        _check(lib().smoe_set_adam(self.h, _ptr(m1), _ptr(m2), int(t)), self.h)
 
     def stats_async(self, dst_ptr: int):
         """smoe_stats_async: enqueue the D2H copy of the last step's raw

@@ -636,3 +636,33 @@ def test_config5_8k_full_size_sampled():
     sampled pixels and one sampled kernel's gradient against the dense oracle
     (every sample is evaluated over all 10^6 kernels)."""
     _sampled_parity("8k", n_px=400, n_kern=2, seed=1)
+
+
+def test_checkpoint_resume():
+    """SURVEY §5 checkpoint/resume: parameters + smoe_get_adam after k steps,
+    restored into a fresh handle, continue like the uninterrupted run (up to
+    the run-to-run rounding of the backward's float atomics), and unlike a
+    restart with fresh optimiser state."""
+    H, W, C, K, T = 48, 64, 3, 90, 12
+    target = torch.as_tensor(synth.image(H, W, C, 71)).cuda()
+    pool = synth.paper_init(target.cpu().numpy(), K, 72, order=1)
+    ha = smoe.SMoE(K, H, W, C, 1, use_graphs=False)
+    pa = dev_pool(pool)
+    for t in range(5):
+        ha.step(pa, target, smoe.LR.paper(t, T), stats=False)
+    m1, m2, tt = ha.get_adam()
+    assert tt == 5
+    saved = pa.clone()
+    for t in range(5, T):
+        ha.step(pa, target, smoe.LR.paper(t, T), stats=False)
+    fresh = saved.clone()
+    hb = smoe.SMoE(K, H, W, C, 1, use_graphs=False)
+    hb.set_adam(m1, m2, tt)
+    hc = smoe.SMoE(K, H, W, C, 1, use_graphs=False)
+    for t in range(5, T):
+        hb.step(saved, target, smoe.LR.paper(t, T), stats=False)
+        hc.step(fresh, target, smoe.LR.paper(t, T), stats=False)
+    torch.cuda.synchronize()
+    d_resume = (saved.flat() - pa.flat()).abs().max().item()
+    d_fresh = (fresh.flat() - pa.flat()).abs().max().item()
+    assert d_resume < 1e-4 and d_fresh > 100 * d_resume, (d_resume, d_fresh)
