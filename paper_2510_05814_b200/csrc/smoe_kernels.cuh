@@ -935,7 +935,8 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
     // inside the ellipse G = sum_c eD_c m_c(x) - K and s = dL/d(d^2) = -g G / 2.
     float eD0[C], eD1[C], K0 = 0.f, K1 = 0.f;
     {
-        double sse = 0.0, ssec = 0.0, unc = 0.0;
+        // lane and warp partials in fp32 (<= 192 terms), block and image sums in fp64
+        float sse = 0.f, ssec = 0.f, unc = 0.f;
         size_t plane = (size_t)A.oH * A.oW;
 #pragma unroll
         for (int c = 0; c < C; c++) {
@@ -944,8 +945,8 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
             float r0 = v0 ? y0[c] - t0 : 0.f, r1 = v1 ? y1[c] - t1 : 0.f;
             float rc0 = v0 ? __saturatef(y0[c]) - __saturatef(t0) : 0.f;
             float rc1 = v1 ? __saturatef(y1[c]) - __saturatef(t1) : 0.f;
-            sse += (double)(r0 * r0) + (double)(r1 * r1);
-            ssec += (double)(rc0 * rc0) + (double)(rc1 * rc1);
+            sse = fmaf(r0, r0, fmaf(r1, r1, sse));
+            ssec = fmaf(rc0, rc0, fmaf(rc1, rc1, ssec));
             eD0[c] = A.e_scale * r0 * iD0;      // 0 if uncovered
             eD1[c] = A.e_scale * r1 * iD1;
             if (!A.rbf) {                       // RBF: dy/dg = m(x), no -y term
@@ -953,14 +954,14 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
                 K1 = fmaf(eD1[c], y1[c], K1);
             }
         }
-        unc = (double)((v0 && D0 <= 0.f) ? 1 : 0) + (double)((v1 && D1 <= 0.f) ? 1 : 0);
+        unc = (float)(((v0 && D0 <= 0.f) ? 1 : 0) + ((v1 && D1 <= 0.f) ? 1 : 0));
 #pragma unroll
         for (int o = 16; o >= 1; o >>= 1) {
             sse += __shfl_xor_sync(FULL, sse, o);
             ssec += __shfl_xor_sync(FULL, ssec, o);
             unc += __shfl_xor_sync(FULL, unc, o);
         }
-        if (lane == 0) { red[0][warp] = sse; red[1][warp] = ssec; red[2][warp] = unc; }
+        if (lane == 0) { red[0][warp] = (double)sse; red[1][warp] = (double)ssec; red[2][warp] = (double)unc; }
         if (MASKS) {
             int c0 = (warp & 1) * 8 + (lane & 7), r0 = (warp >> 1) * 8 + (lane >> 3) * 2;
             float a0[4] = {0.f, 0.f, 0.f, K0}, a1[4] = {0.f, 0.f, 0.f, K1};
