@@ -11,7 +11,7 @@ configuration).  N > 1 (torchrun): tile-row bands per rank, NCCL all-reduce
 of the gradients every step (paper_2510_05814_b200/dist.py).
 
 Timing: W warm-up steps; then K steps, each bracketed by CUDA events on the
-launch stream with an L2 flush (256 MB write) between steps outside the
+launch stream with an L2 flush (256 MB write + 256 MB read) between steps outside the
 events; barrier + synchronize on both sides; max over ranks.  The library's
 own event pairs (smoe_profile_*) time every kernel inside the same region.
 
@@ -202,7 +202,25 @@ def config_dict(name, world):
     return {"workload": f"config{c['cfg']}-{name}", "H": c["H"], "W": c["W"], "C": c["C"], "K": c["K"],
             "expert_order": c["order"], "fit_iterations": c["iters"],
             "parallelism": f"tile-row bands x{world}" if world > 1 else "single GPU",
-            "l2": "flushed between timed steps (256 MB write)"}
+            "l2": "flushed between timed steps (256 MB write, then 256 MB read: the step starts cold and clean)"}
+
+
+class L2Flush:
+    """Evict L2 between timed steps: write a 256 MB buffer (twice the 126 MB
+    L2), then read another one, so the timed step starts with none of its
+    data cached and without the flush's own dirty lines still waiting to be
+    written back (which would otherwise land inside the timed region)."""
+
+    def __init__(self, dev):
+        import torch
+        self.w = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+        self.r = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+        self.s = torch.empty((), dtype=torch.float32, device=dev)
+
+    def __call__(self):
+        import torch
+        self.w.zero_()
+        torch.sum(self.r, dim=0, out=self.s)
 
 
 def main():
@@ -256,7 +274,7 @@ def main():
         else:
             fit.step(params, tgt, lr)
 
-    flush = None if args.no_flush else torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    flush = None if args.no_flush else L2Flush(dev)
     st0 = h.step(params.clone(), tgt, smoe.LR(0, 0, 0, 0, 0), stats=True)   # calibrate capacity
     h.reset_adam()
     for t in range(args.warmup):
@@ -271,7 +289,7 @@ def main():
     torch.cuda.synchronize()
     for i in range(args.steps):
         if flush is not None:
-            flush.zero_()
+            flush()
         ev[i][0].record()
         step(args.warmup + i)
         ev[i][1].record()
@@ -296,7 +314,7 @@ def main():
         torch.cuda.synchronize()
         for i in range(n_prof):
             if flush is not None:
-                flush.zero_()
+                flush()
             step(T_total - 1)
         ktimes, _ = h.profile_end()
 
@@ -313,7 +331,7 @@ def main():
         torch.cuda.synchronize()
         for i in range(nb):
             if flush is not None:
-                flush.zero_()
+                flush()
             step(T_total - 1)
         bt, (tested, hits) = h.profile_end()
         breakdown = {k: v[0] / nb for k, v in bt.items()}
@@ -359,7 +377,7 @@ def main():
             rt = 0.0
             for _ in range(reps):
                 if flush is not None:
-                    flush.zero_()
+                    flush()
                 e0.record()
                 h.render(params, oH, oW, out)
                 e1.record()

@@ -104,6 +104,11 @@ struct Grid {
     int *chunk = nullptr, *hist = nullptr;    // fused binning scratch
     int bin_grid = 0;                         // cooperative grid of k_bin
     bool order_valid = false;                 // LPT order written by the last binning
+    // direct buckets (grids up to SCAN_SINGLE_MAX blocks): block t's list is
+    // ids[t bcap, t bcap + len[t]); otherwise CSR lists ids[start[t], start[t+1])
+    bool direct = false;
+    int bcap = 0;
+    int *len = nullptr;
     long long cap = 0;
     bool calibrated = false;
     GridCtr *gc = nullptr;   // points into Ctl
@@ -243,7 +248,7 @@ void dfree(T *&p)
 void free_grid(Grid &g)
 {
     dfree(g.cnt); dfree(g.start); dfree(g.cursor); dfree(g.order); dfree(g.ids); dfree(g.tmp);
-    dfree(g.lb_state); dfree(g.chunk); dfree(g.hist);
+    dfree(g.lb_state); dfree(g.chunk); dfree(g.hist); dfree(g.len);
     g = Grid();
 }
 
@@ -263,12 +268,22 @@ void ensure_grid(smoe_ctx *h, Grid &g, GridCtr *gc, int oH, int oW)
     long long cap = g.cap;
     bool cal = g.calibrated && g.oH == oH && g.oW == oW;
     dfree(g.cnt); dfree(g.start); dfree(g.cursor); dfree(g.order); dfree(g.lb_state);
-    dfree(g.chunk); dfree(g.hist);
+    dfree(g.chunk); dfree(g.hist); dfree(g.len);
     g.oH = oH; g.oW = oW;
     g.nx = (oW + TILE - 1) / TILE;
     g.ny = (oH + TILE - 1) / TILE;
     g.n_tiles = g.nx * g.ny;
     g.gc = gc;
+    {
+        const char *e = getenv("SMOE_CSR");
+        bool direct = g.n_tiles <= SCAN_SINGLE_MAX && !(e && atoi(e) != 0);
+        if (direct != g.direct) { dfree(g.ids); dfree(g.tmp); cap = 0; cal = false; g.bcap = 0; }
+        g.direct = direct;
+        if (direct) {
+            CK(cudaMalloc(&g.len, sizeof(int) * g.n_tiles));
+            if (!cal) { dfree(g.ids); dfree(g.tmp); cap = 0; g.bcap = 0; }
+        }
+    }
     CK(cudaMalloc(&g.cnt, sizeof(int) * g.n_tiles));
     CK(cudaMalloc(&g.start, sizeof(int) * (g.n_tiles + 1)));
     CK(cudaMalloc(&g.cursor, sizeof(int) * g.n_tiles));
@@ -286,12 +301,20 @@ void ensure_grid(smoe_ctx *h, Grid &g, GridCtr *gc, int oH, int oW)
 void grow(smoe_ctx *h, Grid &g, long long need)
 {
     long long cap = need + need / 4 + 4096;
+    if (g.direct) {
+        // need = the longest bucket; every block gets the same capacity
+        long long b = (need + need / 4 + 32 + 31) / 32 * 32;
+        if (b * g.n_tiles >= (1ll << 31)) throw SmoeError(SMOE_ERR_OUT_OF_MEMORY, "bucket capacity beyond 2^31 ids");
+        g.bcap = (int)b;
+        cap = b * g.n_tiles;
+    }
     dfree(g.ids); dfree(g.tmp);
     CK(cudaMalloc(&g.ids, sizeof(int) * cap));
     CK(cudaMalloc(&g.tmp, sizeof(int) * cap));
     g.cap = cap;
     g.calibrated = true;
     CK(cudaMemsetAsync(&g.gc->need, 0, 2 * sizeof(long long), h->stream));  // need, skipped
+    CK(cudaMemsetAsync(&g.gc->skip, 0, sizeof(unsigned), h->stream));       // the calibrating binning's latch
 }
 
 void read_ctl(smoe_ctx *h)
@@ -358,8 +381,22 @@ void bin_unfused(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_h
                            K, pdev(p), h->R2, sx, sy, g.oW, g.oH, g.nx, ty_lo, ty_hi, h->rec, h->tbox,
                            g.cnt, &h->ctl->hc, g.n_tiles, g.start, g.cursor, g.cap, g.gc,
                            zero_stats ? h->ctl->dstats : nullptr, g.lb_state ? nullptr : g.order, lscale,
-                           use_lpt(g) ? 1 : 0)));
+                           use_lpt(g) ? 1 : 0, g.ids, g.bcap, g.direct ? g.len : nullptr)));
     });
+    if (g.direct) {
+        if (!g.calibrated) {
+            // every slot overflowed (capacity 0): size the buckets from the
+            // longest one, then bin again (the counts were reset)
+            long long cn[2];   // pairs, need
+            CK(cudaMemcpyAsync(cn, &g.gc->pairs, sizeof(cn), cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+            if (&g == &h->train) h->last_pairs = (double)cn[0];
+            grow(h, g, cn[1] > 0 ? cn[1] : 1);
+            return bin_unfused(h, g, p, ty_lo, ty_hi, zero_stats, lscale);
+        }
+        g.order_valid = use_lpt(g);
+        return;
+    }
     if (g.lb_state) {
         int nb2 = (g.n_tiles + LB_CHUNK - 1) / LB_CHUNK;
         launch(h, SMOE_KERNEL_PREPROCESS, "k_scan_lookback", [&] {
@@ -390,7 +427,7 @@ void bin_unfused(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_h
 void bin(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_hi, bool zero_stats, float lscale = 1.0f)
 {
     const char *fe = getenv("SMOE_FUSED_BIN");
-    bool fused = fe ? atoi(fe) != 0 : h->K >= 50000;
+    bool fused = !g.direct && (fe ? atoi(fe) != 0 : h->K >= 50000);
     if (!fused) return bin_unfused(h, g, p, ty_lo, ty_hi, zero_stats, lscale);
     int K = h->K;
     if (!g.bin_grid) {
@@ -490,6 +527,7 @@ void forward_backward(smoe_ctx *h, const smoe_params *p, const float *target)
     if (nt <= 0) return;
     RasterArgs A{};
     A.rec = h->rec; A.ids = g.ids; A.tmp = g.tmp; A.start = g.start; A.gc = g.gc; A.cap = g.cap;
+    A.len = g.direct ? g.len : nullptr; A.bcap = g.bcap;
     A.order = g.order_valid ? g.order : nullptr;
     A.gcw = g.gc; A.n_work = nt; A.n_sm = h->n_sm;
     A.nx = g.nx; A.tile0 = ty_lo * g.nx; A.oW = h->W; A.oH = h->H;
@@ -562,7 +600,7 @@ smoe_status faults(smoe_ctx *h, Grid *g_overflow_report = nullptr)
     Grid *gs[2] = {&h->train, &h->render};
     GridCtr *cs[2] = {&c.train, &c.render};
     for (int i = 0; i < 2; i++) {
-        if (cs[i]->need > gs[i]->cap && gs[i]->ids) {
+        if (cs[i]->need > (gs[i]->direct ? gs[i]->bcap : gs[i]->cap) && gs[i]->ids) {
             long long skipped = cs[i]->skipped;
             grow(h, *gs[i], cs[i]->need);
             set_err(h, "pair capacity exceeded; grown to " + std::to_string(gs[i]->cap) + ", " +
@@ -1008,6 +1046,7 @@ smoe_status smoe_render_ex(smoe_handle h, const smoe_params *p, int out_H, int o
             float *o = odev ? out : stage(h->stage_out, h->stage_out_n, n);
             RasterArgs A{};
             A.rec = h->rec; A.ids = g.ids; A.tmp = g.tmp; A.start = g.start; A.gc = g.gc; A.cap = g.cap;
+            A.len = g.direct ? g.len : nullptr; A.bcap = g.bcap;
             A.order = g.order_valid ? g.order : nullptr; A.gcw = g.gc; A.n_work = g.n_tiles; A.n_sm = h->n_sm;
             A.nx = g.nx; A.tile0 = 0; A.oW = out_W; A.oH = out_H;
             A.sx = (float)h->W / (float)out_W; A.sy = (float)h->H / (float)out_H;
@@ -1058,10 +1097,23 @@ smoe_status smoe_bin(smoe_handle h, const smoe_params *p, int out_H, int out_W, 
         Grid &g = h->render;
         long long P = h->h_ctl->render.pairs;
         if (n_pairs) *n_pairs = P;
-        if (tile_range) CK(cudaMemcpy(tile_range, g.start, sizeof(int) * (g.n_tiles + 1), cudaMemcpyDefault));
-        if (ids) {
-            if (ids_cap < P) throw SmoeError(SMOE_ERR_INVALID_ARG, "smoe_bin: ids_cap < P");
-            CK(cudaMemcpy(ids, g.ids, sizeof(int) * P, cudaMemcpyDefault));
+        if (ids && ids_cap < P) throw SmoeError(SMOE_ERR_INVALID_ARG, "smoe_bin: ids_cap < P");
+        if (g.direct) {
+            // direct buckets -> the CSR form of the ABI
+            std::vector<int> len(g.n_tiles), all((size_t)g.n_tiles * g.bcap), st(g.n_tiles + 1), cs;
+            CK(cudaMemcpy(len.data(), g.len, sizeof(int) * g.n_tiles, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(all.data(), g.ids, sizeof(int) * all.size(), cudaMemcpyDeviceToHost));
+            cs.reserve((size_t)P);
+            for (int t = 0; t < g.n_tiles; t++) {
+                st[t] = (int)cs.size();
+                cs.insert(cs.end(), all.begin() + (size_t)t * g.bcap, all.begin() + (size_t)t * g.bcap + len[t]);
+            }
+            st[g.n_tiles] = (int)cs.size();
+            if (tile_range) CK(cudaMemcpy(tile_range, st.data(), sizeof(int) * st.size(), cudaMemcpyDefault));
+            if (ids && !cs.empty()) CK(cudaMemcpy(ids, cs.data(), sizeof(int) * cs.size(), cudaMemcpyDefault));
+        } else {
+            if (tile_range) CK(cudaMemcpy(tile_range, g.start, sizeof(int) * (g.n_tiles + 1), cudaMemcpyDefault));
+            if (ids) CK(cudaMemcpy(ids, g.ids, sizeof(int) * P, cudaMemcpyDefault));
         }
         if (tilebox) CK(cudaMemcpy(tilebox, h->tbox, sizeof(int4) * h->K, cudaMemcpyDefault));
         return SMOE_OK;

@@ -49,14 +49,14 @@ constexpr int SORT_CAP = 2048;           // bucket size sorted in one smem pass
 // or one render resolution).
 struct GridCtr {
     long long pairs;      // P of the most recent binning on this grid
-    long long need;       // latched: largest P that exceeded the capacity
+    long long need;       // latched: largest P (CSR) / longest bucket (direct) beyond the capacity
     long long skipped;    // latched: sequences skipped because of overflow
     unsigned int ticket;  // last-CTA ticket of k_preprocess
     unsigned int work;    // raster work-queue head (reset by k_preprocess)
     unsigned int scan_vid;   // k_scan_lookback: virtual CTA counter
     unsigned int scan_done;  // k_scan_lookback: finished-CTA ticket
     unsigned int epoch;      // k_scan_lookback: tag of the current scan
-    unsigned int pad2;
+    unsigned int skip;       // 1: the last binning overflowed its capacity (consumers skip)
 };
 
 // Per-handle device counters.
@@ -157,6 +157,7 @@ __device__ __forceinline__ void scan_counts(int *__restrict__ cnt, int n, int *_
         long long P = carry_s;
         start[n] = (int)P;
         gc->pairs = P;
+        gc->skip = P > cap ? 1u : 0u;
         if (P > cap) {
             if (P > gc->need) gc->need = P;
             gc->skipped += 1;
@@ -175,7 +176,8 @@ template <int C, int E>
 __device__ __forceinline__ void
 preprocess_one(int k, ParamsDev p, float R2, float sx, float sy, int oW, int oH,
                int nx, int ty_lo, int ty_hi, float *__restrict__ rec,
-               int4 *__restrict__ tbox, int *__restrict__ cnt, HandleCtr *hc, float lscale)
+               int4 *__restrict__ tbox, int *__restrict__ cnt, HandleCtr *hc, float lscale,
+               bool direct = false, int *__restrict__ dids = nullptr, int bcap = 0)
 {
     using R = Rec<C, E>;
     float2 mu = reinterpret_cast<const float2 *>(p.mu)[k];
@@ -213,13 +215,100 @@ preprocess_one(int k, ParamsDev p, float R2, float sx, float sy, int oW, int oH,
     if (ok && xl <= xh && yl <= yh) {
         tb = make_int4((int)xl / TILE, (int)xh / TILE, (int)yl / TILE, (int)yh / TILE);
         int y0 = max(tb.z, ty_lo), y1 = min(tb.w, ty_hi - 1);
-        for (int ty = y0; ty <= y1; ty++)
-            for (int tx = tb.x; tx <= tb.y; tx++) atomicAdd(&cnt[ty * nx + tx], 1);
+        if (direct) {
+            // direct buckets: the count atomic returns k's slot in block t's
+            // fixed-capacity bucket (four atomics in flight per round)
+            const int wx = tb.y - tb.x + 1, nbx = max(0, y1 - y0 + 1) * wx;
+            for (int i0 = 0; i0 < nbx; i0 += 4) {
+                int t[4], sl[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const int i = i0 + q, yy = y0 + i / wx, xx = tb.x + i % wx;
+                    t[q] = yy * nx + xx;
+                    sl[q] = i < nbx ? atomicAdd(&cnt[t[q]], 1) : bcap;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; q++)
+                    if (sl[q] < bcap) dids[(size_t)t[q] * bcap + sl[q]] = k;
+            }
+        } else {
+            for (int ty = y0; ty <= y1; ty++)
+                for (int tx = tb.x; tx <= tb.y; tx++) atomicAdd(&cnt[ty * nx + tx], 1);
+        }
     }
     tbox[k] = tb;
 }
 
 constexpr int PRE_NT = 256;
+
+// Direct buckets (a1 + a3 in one pass, small grids): kernel k's id went
+// straight into the slot its count atomic returned in block t's fixed-capacity
+// bucket ids[t * bcap, ...).  The last CTA of k_preprocess publishes the
+// bucket lengths (len), P and the largest bucket, latches overflow (a bucket
+// longer than bcap: consumers skip, the host regrows), zeroes the counts and
+// the loss partials, and builds the LPT order of the band's blocks.
+__device__ __forceinline__ void finish_direct(int *__restrict__ cnt, int n, int *__restrict__ len, int bcap,
+                                              GridCtr *gc, double *dstats, int *__restrict__ order, int t0,
+                                              int nt)
+{
+    __shared__ unsigned long long sP;
+    __shared__ int sMax;
+    __shared__ int hist[256];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) { sP = 0ull; sMax = 0; }
+    if (tid < 4 && dstats) dstats[tid] = 0.0;
+    hist[tid] = 0;
+    __syncthreads();
+    unsigned long long p = 0;
+    int mx = 0;
+    for (int i = tid; i < n; i += PRE_NT) {
+        const int c = __ldcg(cnt + i);
+        len[i] = c;
+        cnt[i] = 0;
+        p += (unsigned)c;
+        mx = max(mx, c);
+        if (order && i >= t0 && i < t0 + nt) atomicAdd(&hist[255 - min(c, 255)], 1);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        p += __shfl_xor_sync(FULL, p, o);
+        mx = max(mx, __shfl_xor_sync(FULL, mx, o));
+    }
+    if (lane == 0) { atomicAdd(&sP, p); atomicMax(&sMax, mx); }
+    __syncthreads();
+    if (tid == 0) {
+        const long long P = (long long)sP;
+        gc->pairs = P;
+        const bool ovf = sMax > bcap;
+        gc->skip = ovf ? 1u : 0u;
+        if (ovf) {
+            if (sMax > gc->need) gc->need = sMax;
+            gc->skipped += 1;
+        }
+    }
+    if (!order) return;
+    {
+        int v = hist[tid], inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(FULL, inc, o);
+            if (lane >= o) inc += t;
+        }
+        __shared__ int wt[PRE_NT / 32];
+        if (lane == 31) wt[wid] = inc;
+        __syncthreads();
+        int pre = 0;
+        for (int w = 0; w < wid; w++) pre += wt[w];
+        __syncthreads();
+        hist[tid] = pre + inc - v;
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += PRE_NT) {
+        if (i < t0 || i >= t0 + nt) continue;
+        const int c = len[i];             // this thread's own write above
+        order[atomicAdd(&hist[255 - min(c, 255)], 1)] = i;
+    }
+}
 
 template <int C, int E>
 __global__ void __launch_bounds__(PRE_NT)
@@ -227,10 +316,13 @@ k_preprocess(int K, ParamsDev p, float R2, float sx /* oW/W */, float sy /* oH/H
              int nx, int ty_lo, int ty_hi, float *__restrict__ rec,
              int4 *__restrict__ tbox, int *__restrict__ cnt, HandleCtr *hc,
              int n_tiles, int *__restrict__ start, int *__restrict__ cursor, long long cap,
-             GridCtr *gc, double *dstats, int *__restrict__ order, float lscale, int build_order)
+             GridCtr *gc, double *dstats, int *__restrict__ order, float lscale, int build_order,
+             int *__restrict__ dids, int bcap, int *__restrict__ len)
 {
     int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k < K) preprocess_one<C, E>(k, p, R2, sx, sy, oW, oH, nx, ty_lo, ty_hi, rec, tbox, cnt, hc, lscale);
+    if (k < K)
+        preprocess_one<C, E>(k, p, R2, sx, sy, oW, oH, nx, ty_lo, ty_hi, rec, tbox, cnt, hc, lscale, len != nullptr,
+                             dids, bcap);
     if (!order) return;   // large grid: k_scan_lookback follows
     // the last CTA to finish scans the counts (a2)
     __shared__ bool last;
@@ -242,6 +334,12 @@ k_preprocess(int K, ParamsDev p, float R2, float sx /* oW/W */, float sy /* oH/H
     __syncthreads();
     if (!last) return;
     __threadfence();
+    if (len) {
+        finish_direct(cnt, n_tiles, len, bcap, gc, dstats, build_order ? order : nullptr, ty_lo * nx,
+                      (ty_hi - ty_lo) * nx);
+        if (threadIdx.x == 0) { gc->ticket = 0; gc->work = 0; }
+        return;
+    }
     scan_counts<PRE_NT>(cnt, n_tiles, start, cursor, cap, gc, dstats);
     if (!build_order) {
         if (threadIdx.x == 0) { gc->ticket = 0; gc->work = 0; }
@@ -369,6 +467,7 @@ k_scan_lookback(int *__restrict__ cnt, int n, int *__restrict__ start, int *__re
         long long P = excl_s + agg;
         start[n] = (int)P;
         gc->pairs = P;
+        gc->skip = P > cap ? 1u : 0u;
         if (P > cap) {
             if (P > gc->need) gc->need = P;
             gc->skipped += 1;
@@ -392,7 +491,7 @@ __global__ void __launch_bounds__(64)
 k_scatter(int K, const int4 *__restrict__ tbox, int nx, int ty_lo, int ty_hi,
           int *__restrict__ cursor, int *__restrict__ ids, long long cap, const GridCtr *gc)
 {
-    if (gc->pairs > cap) return;
+    if (gc->skip) return;
     int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= K) return;
     int4 tb = tbox[k];
@@ -531,6 +630,7 @@ k_bin(BinArgs B)
         const long long P = carry;
         B.start[n] = (int)P;
         B.gc->pairs = P;
+        B.gc->skip = P > B.cap ? 1u : 0u;
         if (P > B.cap) {
             if (P > B.gc->need) B.gc->need = P;
             B.gc->skipped += 1;
@@ -727,7 +827,9 @@ struct RasterArgs {
     const float *rec;
     int *ids;             // block lists (bucket-sorted in place by the raster)
     int *tmp;             // merge scratch for buckets larger than the smem chunk
-    const int *start;
+    const int *start;     // CSR lists: block t = ids[start[t], start[t+1])
+    const int *len;       // direct buckets (len != null): block t = ids[t bcap, t bcap + len[t])
+    int bcap;
     const GridCtr *gc;
     long long cap;
     int nx, tile0;
@@ -817,7 +919,8 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
     const float xs = (px + 0.5f) * A.sx - 0.5f;
     const float ys0 = (py0 + 0.5f) * A.sy - 0.5f, ys1 = (py1 + 0.5f) * A.sy - 0.5f;
     const float R2 = A.R2;
-    const int s0 = A.start[tile], n = A.start[tile + 1] - s0;
+    const int s0 = A.len ? tile * A.bcap : A.start[tile];
+    const int n = A.len ? A.len[tile] : A.start[tile + 1] - s0;
     // a4 (second digit): sort this block's bucket by kernel id; srec doubles
     // as the shared scratch (its capacity in ints is a power of two >= 1024)
     constexpr int SCHUNK = (BATCH * RS4 * 4 >= 2048) ? 2048 : 1024;
@@ -1165,7 +1268,7 @@ template <int C, int E, bool TRAIN, bool PROF, bool KPAR>
 __global__ void __launch_bounds__(128, KPAR ? (E == 3 ? SMOE_KPAR_MINB : SMOE_KPAR_MINB_CONST) : 12)
 k_raster(RasterArgs A)
 {
-    if (A.gc->pairs > A.cap) return;
+    if (A.gc->skip) return;
     int i = blockIdx.x;
     const int k = i / A.n_sm, j = i - k * A.n_sm;
     if ((k & 1) && (k + 1) * A.n_sm <= A.n_work) i = k * A.n_sm + (A.n_sm - 1 - j);
@@ -1194,7 +1297,7 @@ k_adam(int K, ParamsMut p, float *__restrict__ acc, const float *__restrict__ gr
 {
     using R = Rec<C, E>;
     constexpr int P = R::P;
-    if (MODE != 2 && gc->pairs > cap) return;
+    if (MODE != 2 && gc->skip) return;
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const bool live = k < K;
     const long long t = hc->t + 1;
