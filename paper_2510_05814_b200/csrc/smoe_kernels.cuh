@@ -95,6 +95,16 @@ __device__ __forceinline__ float ex2_approx(float x)
 
 __device__ __forceinline__ bool finitef(float x) { return isfinite(x); }
 
+// gpu-scope acq_rel add (one release of the CTA's prior writes after a
+// barrier, one acquire for what follows; cheaper than __threadfence(), a
+// sequentially consistent fence plus an L1 invalidation)
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned *p, unsigned v)
+{
+    unsigned r;
+    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+    return r;
+}
+
 // ------------------------------------------------------------ a2 / a4 -----
 // Exclusive scan of the per-block counts by one CTA of NT threads (4 counts
 // per thread per round).  Produces start[n+1] and the scatter cursors, zeroes
@@ -325,15 +335,13 @@ k_preprocess(int K, ParamsDev p, float R2, float sx /* oW/W */, float sy /* oH/H
                              dids, bcap);
     if (!order) return;   // large grid: k_scan_lookback follows
     // the last CTA to finish scans the counts (a2)
+    // (grid-sync pattern: barrier, then one acq_rel ticket by thread 0; the
+    // last CTA reads the counts from L2)
     __shared__ bool last;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        last = atomicAdd(&gc->ticket, 1u) == gridDim.x - 1;
-    }
+    if (threadIdx.x == 0) last = atom_add_acq_rel_gpu(&gc->ticket, 1u) == gridDim.x - 1;
     __syncthreads();
     if (!last) return;
-    __threadfence();
     if (len) {
         finish_direct(cnt, n_tiles, len, bcap, gc, dstats, build_order ? order : nullptr, ty_lo * nx,
                       (ty_hi - ty_lo) * nx);
@@ -1384,16 +1392,13 @@ k_adam(int K, ParamsMut p, float *__restrict__ acc, const float *__restrict__ gr
         }
     }
     if (MODE == 1) return;
-    // the last CTA advances the step counter after every CTA has read it
+    // the last CTA advances the step counter after every CTA has read it (the
+    // reads were consumed before the barrier; no other data is published, so
+    // a relaxed ticket suffices and no CTA waits for its stores to drain)
     __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        unsigned int ticket = atomicAdd(&hc->done, 1u);
-        if (ticket == gridDim.x - 1) {
-            hc->t = t;
-            hc->done = 0;
-            __threadfence();
-        }
+    if (threadIdx.x == 0 && atomicAdd(&hc->done, 1u) == gridDim.x - 1) {
+        hc->t = t;
+        hc->done = 0;
     }
 }
 
