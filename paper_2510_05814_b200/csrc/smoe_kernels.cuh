@@ -271,13 +271,22 @@ __device__ __forceinline__ void finish_direct(int *__restrict__ cnt, int n, int 
     __syncthreads();
     unsigned long long p = 0;
     int mx = 0;
-    for (int i = tid; i < n; i += PRE_NT) {
-        const int c = __ldcg(cnt + i);
-        len[i] = c;
-        cnt[i] = 0;
-        p += (unsigned)c;
-        mx = max(mx, c);
-        if (order && i >= t0 && i < t0 + nt) atomicAdd(&hist[255 - min(c, 255)], 1);
+    constexpr int U = 8;   // counts in flight per thread
+    for (int base = tid; base < n; base += U * PRE_NT) {
+        int c[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) c[q] = base + q * PRE_NT < n ? __ldcg(cnt + base + q * PRE_NT) : 0;
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            const int i = base + q * PRE_NT;
+            if (i < n) {
+                len[i] = c[q];
+                cnt[i] = 0;
+                p += (unsigned)c[q];
+                mx = max(mx, c[q]);
+                if (order && i >= t0 && i < t0 + nt) atomicAdd(&hist[255 - min(c[q], 255)], 1);
+            }
+        }
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
@@ -313,10 +322,15 @@ __device__ __forceinline__ void finish_direct(int *__restrict__ cnt, int n, int 
         hist[tid] = pre + inc - v;
     }
     __syncthreads();
-    for (int i = tid; i < n; i += PRE_NT) {
-        if (i < t0 || i >= t0 + nt) continue;
-        const int c = len[i];             // this thread's own write above
-        order[atomicAdd(&hist[255 - min(c, 255)], 1)] = i;
+    for (int base = tid; base < n; base += U * PRE_NT) {
+        int c[U];
+#pragma unroll
+        for (int q = 0; q < U; q++) c[q] = base + q * PRE_NT < n ? len[base + q * PRE_NT] : 0;   // own writes
+#pragma unroll
+        for (int q = 0; q < U; q++) {
+            const int i = base + q * PRE_NT;
+            if (i < n && i >= t0 && i < t0 + nt) order[atomicAdd(&hist[255 - min(c[q], 255)], 1)] = i;
+        }
     }
 }
 
