@@ -34,9 +34,6 @@ constexpr int TILE = 16;                 // 16x16 blocks
 #ifndef SMOE_KPAR_MINB_CONST
 #define SMOE_KPAR_MINB_CONST 7           // ... constant experts (fewer live sums, no spills at 7)
 #endif
-#ifndef SMOE_FWD_UNROLL
-#define SMOE_FWD_UNROLL 1                // forward kernel-loop unroll
-#endif
 #ifndef SMOE_RASTER_BATCH
 #define SMOE_RASTER_BATCH 128            // kernel records staged per shared-memory batch
 #endif
