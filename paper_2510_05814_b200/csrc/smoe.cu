@@ -549,12 +549,27 @@ void forward_backward(smoe_ctx *h, const smoe_params *p, const float *target)
     });
 }
 
+// k_adam (element-parallel) while one wave of resident CTAs (8 per SM)
+// covers every (kernel, slot) element, else k_adam_kt (one thread per kernel)
+static bool adam_elementwise(smoe_ctx *h)
+{
+    int v = 0;
+    DISPATCH_CE(h, (v = Rec<C_, E_>::V));
+    return (long long)h->K <= 8LL * h->n_sm * (ADAM_NT / v);
+}
+
 void *adam_func(smoe_ctx *h, int mode)
 {
     void *f = nullptr;
-    if (mode == 0) DISPATCH_CE(h, (f = (void *)k_adam<C_, E_, 0>));
-    else if (mode == 1) DISPATCH_CE(h, (f = (void *)k_adam<C_, E_, 1>));
-    else DISPATCH_CE(h, (f = (void *)k_adam<C_, E_, 2>));
+    if (adam_elementwise(h)) {
+        if (mode == 0) DISPATCH_CE(h, (f = (void *)k_adam<C_, E_, 0>));
+        else if (mode == 1) DISPATCH_CE(h, (f = (void *)k_adam<C_, E_, 1>));
+        else DISPATCH_CE(h, (f = (void *)k_adam<C_, E_, 2>));
+    } else {
+        if (mode == 0) DISPATCH_CE(h, (f = (void *)k_adam_kt<C_, E_, 0>));
+        else if (mode == 1) DISPATCH_CE(h, (f = (void *)k_adam_kt<C_, E_, 1>));
+        else DISPATCH_CE(h, (f = (void *)k_adam_kt<C_, E_, 2>));
+    }
     return f;
 }
 
@@ -581,7 +596,16 @@ void launch_adam(smoe_ctx *h, int mode, const smoe_params *p, const float *grad_
     AdamArgs a;
     adam_args(h, p, grad_in, grad_out, lr, a);
     void *f = adam_func(h, mode);
-    dim3 grid((h->K + 63) / 64), block(64);
+    dim3 grid, block;
+    if (adam_elementwise(h)) {
+        int kpb = 0;
+        DISPATCH_CE(h, (kpb = ADAM_NT / Rec<C_, E_>::V));
+        grid = dim3((h->K + kpb - 1) / kpb);
+        block = dim3(ADAM_NT);
+    } else {
+        grid = dim3((h->K + 63) / 64);
+        block = dim3(64);
+    }
     launch(h, SMOE_KERNEL_ADAM, "k_adam", [&] {
         (void)cudaLaunchKernel(f, grid, block, a.ptrs, 0, h->stream);
     });

@@ -26,7 +26,7 @@ namespace smoe {
 constexpr int TILE = 16;                 // 16x16 blocks
 // build-time tuning knobs (A/B builds in scripts/; defaults are the tuned values)
 #ifndef SMOE_FWD_UNROLL
-#define SMOE_FWD_UNROLL 1                // forward kernel-loop unroll
+#define SMOE_FWD_UNROLL 1                // forward kernel-loop unroll (x4 constant experts, x2 kernel-parallel train)
 #endif
 #ifndef SMOE_KPAR_MINB
 #define SMOE_KPAR_MINB 6                 // kernel-parallel raster, linear experts: min CTAs/SM
@@ -37,7 +37,11 @@ constexpr int TILE = 16;                 // 16x16 blocks
 #ifndef SMOE_RASTER_BATCH
 #define SMOE_RASTER_BATCH 128            // kernel records staged per shared-memory batch
 #endif
+#ifndef SMOE_BWD_TWO
+#define SMOE_BWD_TWO 0                   // kernel-parallel backward: two list entries per iteration
+#endif
 constexpr int kFwdUnroll = SMOE_FWD_UNROLL;
+constexpr bool BWD_TWO = SMOE_BWD_TWO != 0;
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int SORT_CAP = 2048;           // bucket size sorted in one smem pass
@@ -919,15 +923,19 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
     using R = Rec<C, E>;
     constexpr int RS4 = R::RS / 4;
     constexpr int BATCH = SMOE_RASTER_BATCH;
-    // forward kernel-loop unroll: 4 for constant experts (+2% at config 3),
-    // none for linear ones (register spills at 80 registers)
-    constexpr int FWD_UNROLL = (E == 3) ? kFwdUnroll : 4 * kFwdUnroll;
+    // forward kernel-loop unroll: 4 for constant experts (+2% at config 3);
+    // linear ones: 2 in the kernel-parallel train raster (+2% at config 2),
+    // none in the 40-register forms (spills)
     constexpr bool MASKS = TRAIN && KPAR;
+    constexpr int FWD_UNROLL = (E == 3) ? (MASKS ? 2 : 1) * kFwdUnroll : 4 * kFwdUnroll;
     __shared__ float4 srec[BATCH * RS4];
     __shared__ int sid[BATCH];
-    __shared__ float4 spix[MASKS ? 256 : 1];      // eD_0..eD_{C-1}, K  (C <= 3)
+    // per-lane backward seeds of the lane's pixel pair, packed by pixel:
+    // [warp][lane] = {(eD_0, eD_0'), (eD_1, eD_1')}, {(eD_2, eD_2'), (K, K')}
+    __shared__ float4 spix[MASKS ? 256 : 1];
     constexpr int CAPW = 2048;                    // per-warp pair-list capacity (window)
-    __shared__ unsigned short spw[MASKS ? 4 : 1][MASKS ? CAPW : 1];   // (kernel << 8) | pixel
+    // list entry: (kernel << 7) | (lane << 2) | (lower pixel hit << 1) | upper pixel hit
+    __shared__ unsigned short spw[MASKS ? 4 : 1][MASKS ? CAPW : 1];
     __shared__ double red[3][4];
 
     const int tx = tile % A.nx, ty = tile / A.nx;
@@ -951,7 +959,7 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
     unsigned long long w_tested = 0, w_hit = 0;
     int wrun = 0;                                  // pairs this warp listed (KPAR)
     const unsigned lt = (1u << lane) - 1u;
-    const int pix0 = ((warp >> 1) * 8 + (lane >> 3) * 2) * 16 + (warp & 1) * 8 + (lane & 7);
+    const unsigned ebits = (unsigned)lane << 2;
     const int w_valid = PROF ? __popc(__ballot_sync(FULL, v0)) + __popc(__ballot_sync(FULL, v1)) : 0;
 
     auto load_batch = [&](int b0, int nb) {
@@ -1004,12 +1012,13 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
             }
             if ((b0m | b1m) == 0u) continue;
             if (MASKS && n <= BATCH) {
-                // this warp's pairs of kernel j, appended to its list
-                const int c0 = __popc(b0m);
-                const int p0 = wrun + __popc(b0m & lt), p1 = wrun + c0 + __popc(b1m & lt);
-                if (h0 && p0 < CAPW) spw[warp][p0] = (unsigned short)((j << 8) | pix0);
-                if (h1 && p1 < CAPW) spw[warp][p1] = (unsigned short)((j << 8) | (pix0 + 16));
-                wrun += c0 + __popc(b1m);
+                // this warp's lanes with a pixel inside kernel j's ellipse,
+                // appended to its list (one entry per lane = pixel pair)
+                const unsigned bm = b0m | b1m;
+                const int p0 = wrun + __popc(bm & lt);
+                if ((h0 || h1) && p0 < CAPW)
+                    spw[warp][p0] = (unsigned short)(((unsigned)j << 7) | ebits | (h1 ? 2u : 0u) | (h0 ? 1u : 0u));
+                wrun += __popc(bm);
             }
             const float2 ea = __ffma2_rn(q, make_float2(-0.5f * LOG2E, -0.5f * LOG2E), make_float2(r[5], r[5]));
             const float2 g = make_float2(h0 ? ex2_approx(ea.x) : 0.f, h1 ? ex2_approx(ea.y) : 0.f);
@@ -1085,12 +1094,11 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
         }
         if (lane == 0) { red[0][warp] = (double)sse; red[1][warp] = (double)ssec; red[2][warp] = (double)unc; }
         if (MASKS) {
-            int c0 = (warp & 1) * 8 + (lane & 7), r0 = (warp >> 1) * 8 + (lane >> 3) * 2;
             float a0[4] = {0.f, 0.f, 0.f, K0}, a1[4] = {0.f, 0.f, 0.f, K1};
 #pragma unroll
             for (int c = 0; c < C; c++) { a0[c] = eD0[c]; a1[c] = eD1[c]; }
-            spix[r0 * 16 + c0] = make_float4(a0[0], a0[1], a0[2], a0[3]);
-            spix[(r0 + 1) * 16 + c0] = make_float4(a1[0], a1[1], a1[2], a1[3]);
+            spix[2 * threadIdx.x] = make_float4(a0[0], a1[0], a0[1], a1[1]);
+            spix[2 * threadIdx.x + 1] = make_float4(a0[2], a1[2], a0[3], a1[3]);
         }
         __syncthreads();
         if (threadIdx.x < 3) {
@@ -1154,14 +1162,18 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
     }
 
     // ---- kernel-parallel backward over per-warp pair lists ----
-    // Each warp owns the (kernel, pixel) pairs of its 8x8 quadrant that lie
-    // inside the kernel's ellipse, listed kernel-major in shared memory (the
-    // forward wrote them while testing; larger K_n rebuild them per batch).
-    // The warp's 32 lanes split the list into equal contiguous ranges, so
-    // every lane carries the same number of pairs; a lane accumulates the
-    // raw sums of the current kernel in registers and flushes them with
-    // vector atomics when the kernel changes and at the end of its range.
-    const float tx0 = (float)(tx * TILE), ty0f = (float)(ty * TILE);
+    // Each warp owns the (kernel, lane) entries of its 8x8 quadrant whose
+    // lane has a pixel inside the kernel's ellipse, listed kernel-major in
+    // shared memory (the forward wrote them while testing; larger K_n rebuild
+    // them per batch).  An entry is the lane's vertical pixel pair (shared
+    // dx, packed f32x2 in dy; a pixel outside the ellipse gets g = 0, so it
+    // adds nothing).  The warp's 32 lanes split the list into
+    // equal contiguous ranges, so every lane carries the same number of
+    // entries; a lane accumulates the raw sums of the current kernel in
+    // registers and flushes them with vector atomics when the kernel changes
+    // and at the end of its range.
+    const float xw = (float)(tx * TILE + (warp & 1) * 8), yw = (float)(ty * TILE + (warp >> 1) * 8);
+    const float4 *spw_pix = spix + warp * 64;   // this warp's lanes' seeds
     for (int b0 = 0; b0 < n; b0 += BATCH) {
         int nb = min(BATCH, n - b0);
         int total = wrun;                      // n <= BATCH: listed by the forward
@@ -1169,7 +1181,7 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
         for (int q0 = 0; q0 < total || (n > BATCH && q0 == 0); q0 += CAPW) {
             if (n > BATCH || q0 > 0) {
                 // (re)build the warp's list window [q0, q0 + CAPW) for the
-                // resident batch: the cull test again, pairs in window kept
+                // resident batch: the cull test again, entries in window kept
                 int run = 0;
                 for (int j = 0; j < nb; j++) {
                     float rb[R::RS];
@@ -1178,11 +1190,11 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
                     float2 dyv, wv, qv;
                     dist2(rb, dx, dyv, u, wv, qv);
                     bool h0 = v0 && qv.x <= R2, h1 = v1 && qv.y <= R2;
-                    unsigned b0m = __ballot_sync(FULL, h0), b1m = __ballot_sync(FULL, h1);
-                    int p0 = run + __popc(b0m & lt) - q0, p1 = run + __popc(b0m) + __popc(b1m & lt) - q0;
-                    if (h0 && p0 >= 0 && p0 < CAPW) spw[warp][p0] = (unsigned short)((j << 8) | pix0);
-                    if (h1 && p1 >= 0 && p1 < CAPW) spw[warp][p1] = (unsigned short)((j << 8) | (pix0 + 16));
-                    run += __popc(b0m) + __popc(b1m);
+                    const unsigned bm = __ballot_sync(FULL, h0 || h1);
+                    const int p0 = run + __popc(bm & lt) - q0;
+                    if ((h0 || h1) && p0 >= 0 && p0 < CAPW)
+                        spw[warp][p0] = (unsigned short)(((unsigned)j << 7) | ebits | (h1 ? 2u : 0u) | (h0 ? 1u : 0u));
+                    run += __popc(bm);
                 }
                 total = run;
                 __syncwarp();
@@ -1193,82 +1205,92 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
             int cj = -1;
             float4 *dst = nullptr;
             float r[R::RS];
-            // two list entries of the same kernel per iteration, as a packed
-            // f32x2 pair (the second slot is a null pixel, eD = K = 0, when
-            // the next entry is past the range or of another kernel)
-            float2 acc[R::P];
+            float acc[R::P];
 #pragma unroll
-            for (int i = 0; i < R::P; i++) acc[i] = make_float2(0.f, 0.f);
+            for (int i = 0; i < R::P; i++) acc[i] = 0.f;
+            // one entry's contribution to the raw sums (a pixel outside the ellipse: g = 0)
+            auto add_entry = [&](const unsigned e) {
+                const int l = (int)((e >> 2) & 31u);
+                    const float4 pa = spw_pix[2 * l], pb = spw_pix[2 * l + 1];
+                    const float dx = xw + (float)(l & 7) - r[0];
+                    const float yl = yw + (float)((l >> 3) * 2) - r[1];
+                    const float2 dy = make_float2(yl, yl + 1.0f);
+                    const float u = r[2] * dx;
+                    const float bdx = r[3] * dx;
+                    const float2 v = __ffma2_rn(make_float2(r[4], r[4]), dy, make_float2(bdx, bdx));
+                    const float uu = u * u;
+                    const float2 qd = __ffma2_rn(v, v, make_float2(uu, uu));
+                    const float2 ea = __ffma2_rn(qd, make_float2(-0.5f * LOG2E, -0.5f * LOG2E), make_float2(r[5], r[5]));
+                    const float2 g = make_float2((e & 1u) ? ex2_approx(ea.x) : 0.f, (e & 2u) ? ex2_approx(ea.y) : 0.f);
+                    const float2 eda[4] = {make_float2(pa.x, pa.y), make_float2(pa.z, pa.w),
+                                           make_float2(pb.x, pb.y), make_float2(pb.z, pb.w)};
+                    float2 Gs = make_float2(-eda[3].x, -eda[3].y);
+    #pragma unroll
+                    for (int c = 0; c < C; c++) {
+                        float2 mc = make_float2(r[6 + c * E], r[6 + c * E]);
+                        if (E == 3) {
+                            const float mb = fmaf(r[6 + c * E + 1], dx, r[6 + c * E]);
+                            mc = __ffma2_rn(make_float2(r[6 + c * E + 2], r[6 + c * E + 2]), dy, make_float2(mb, mb));
+                        }
+                        Gs = __ffma2_rn(eda[c], mc, Gs);
+                        const float2 ge = __fmul2_rn(g, eda[c]);
+                        const float gsum = ge.x + ge.y;
+                        acc[6 + c * E] += gsum;
+                        if (E == 3) {
+                            acc[6 + c * E + 1] = fmaf(gsum, dx, acc[6 + c * E + 1]);
+                            acc[6 + c * E + 2] = fmaf(ge.x, dy.x, fmaf(ge.y, dy.y, acc[6 + c * E + 2]));
+                        }
+                    }
+                    const float2 sg = __fmul2_rn(__fmul2_rn(make_float2(-0.5f, -0.5f), g), Gs);
+                    const float ssum = sg.x + sg.y;
+                    const float2 sv = __fmul2_rn(sg, v);
+                    const float svsum = sv.x + sv.y;
+                    acc[0] = fmaf(ssum, u, acc[0]);
+                    acc[1] += svsum;
+                    acc[2] = fmaf(ssum, u * dx, acc[2]);
+                    acc[3] = fmaf(svsum, dx, acc[3]);
+                    acc[4] = fmaf(sv.x, dy.x, fmaf(sv.y, dy.y, acc[4]));
+                    acc[5] += ssum;
+            };
             for (int q = lo; q < hi;) {
                 const unsigned e = spw[warp][q];
-                const int j = (int)(e >> 8), pa = (int)(e & 255u);
+                const int j = (int)(e >> 7);
                 if (j != cj) {
                     if (cj >= 0) {
 #pragma unroll
                         for (int q4 = 0; q4 < (R::P + 3) / 4; q4++) {
                             float t4[4];
 #pragma unroll
-                            for (int k4 = 0; k4 < 4; k4++)
-                                t4[k4] = (4 * q4 + k4 < R::P) ? acc[4 * q4 + k4].x + acc[4 * q4 + k4].y : 0.f;
+                            for (int k4 = 0; k4 < 4; k4++) t4[k4] = (4 * q4 + k4 < R::P) ? acc[4 * q4 + k4] : 0.f;
                             atomicAdd(dst + q4, make_float4(t4[0], t4[1], t4[2], t4[3]));
                         }
 #pragma unroll
-                        for (int i = 0; i < R::P; i++) acc[i] = make_float2(0.f, 0.f);
+                        for (int i = 0; i < R::P; i++) acc[i] = 0.f;
                     }
                     cj = j;
                     dst = reinterpret_cast<float4 *>(A.acc + (size_t)sid[j] * R::V);
                     load_rec(j, r);
                 }
-                unsigned e2 = (q + 1 < hi) ? spw[warp][q + 1] : 0xffffu;
-                const bool two = (int)(e2 >> 8) == j;
-                const int pb = two ? (int)(e2 & 255u) : pa;
-                q += two ? 2 : 1;
-                const float4 pda = spix[pa];
-                float4 pdb = spix[pb];
-                if (!two) pdb = make_float4(0.f, 0.f, 0.f, 0.f);
-                const float2 x2 = make_float2(tx0 + (float)(pa & 15), tx0 + (float)(pb & 15));
-                const float2 y2 = make_float2(ty0f + (float)(pa >> 4), ty0f + (float)(pb >> 4));
-                const float2 dx = __fadd2_rn(x2, make_float2(-r[0], -r[0]));
-                const float2 dy = __fadd2_rn(y2, make_float2(-r[1], -r[1]));
-                const float2 u = __fmul2_rn(make_float2(r[2], r[2]), dx);
-                const float2 v = __ffma2_rn(make_float2(r[3], r[3]), dx, __fmul2_rn(make_float2(r[4], r[4]), dy));
-                const float2 qd = __ffma2_rn(v, v, __fmul2_rn(u, u));
-                const float2 ea = __ffma2_rn(qd, make_float2(-0.5f * LOG2E, -0.5f * LOG2E), make_float2(r[5], r[5]));
-                const float2 g = make_float2(ex2_approx(ea.x), ex2_approx(ea.y));
-                const float2 eda[4] = {make_float2(pda.x, pdb.x), make_float2(pda.y, pdb.y),
-                                       make_float2(pda.z, pdb.z), make_float2(pda.w, pdb.w)};
-                float2 Gs = make_float2(-eda[3].x, -eda[3].y);
-#pragma unroll
-                for (int c = 0; c < C; c++) {
-                    float2 mc = make_float2(r[6 + c * E], r[6 + c * E]);
-                    if (E == 3) {
-                        mc = __ffma2_rn(make_float2(r[6 + c * E + 1], r[6 + c * E + 1]), dx, mc);
-                        mc = __ffma2_rn(make_float2(r[6 + c * E + 2], r[6 + c * E + 2]), dy, mc);
-                    }
-                    Gs = __ffma2_rn(eda[c], mc, Gs);
-                    const float2 ge = __fmul2_rn(g, eda[c]);
-                    acc[6 + c * E] = __fadd2_rn(acc[6 + c * E], ge);
-                    if (E == 3) {
-                        acc[6 + c * E + 1] = __ffma2_rn(ge, dx, acc[6 + c * E + 1]);
-                        acc[6 + c * E + 2] = __ffma2_rn(ge, dy, acc[6 + c * E + 2]);
-                    }
+                if (BWD_TWO) {
+                    // a second entry of the same kernel in the same iteration
+                    // (or a null one: same lane, no pixel)
+                    unsigned e2 = (q + 1 < hi) ? spw[warp][q + 1] : 0u;
+                    const bool two = q + 1 < hi && (int)(e2 >> 7) == j;
+                    if (!two) e2 = e & ~3u;
+                    q += two ? 2 : 1;
+                    add_entry(e);
+                    add_entry(e2);
+                } else {
+                    q++;
+                    add_entry(e);
                 }
-                const float2 sg = __fmul2_rn(__fmul2_rn(make_float2(-0.5f, -0.5f), g), Gs);
-                const float2 su = __fmul2_rn(sg, u), sv = __fmul2_rn(sg, v);
-                acc[0] = __fadd2_rn(acc[0], su);
-                acc[1] = __fadd2_rn(acc[1], sv);
-                acc[2] = __ffma2_rn(su, dx, acc[2]);
-                acc[3] = __ffma2_rn(sv, dx, acc[3]);
-                acc[4] = __ffma2_rn(sv, dy, acc[4]);
-                acc[5] = __fadd2_rn(acc[5], sg);
             }
             if (cj >= 0) {
 #pragma unroll
                 for (int q4 = 0; q4 < (R::P + 3) / 4; q4++) {
                     float t4[4];
 #pragma unroll
-                    for (int k4 = 0; k4 < 4; k4++)
-                        t4[k4] = (4 * q4 + k4 < R::P) ? acc[4 * q4 + k4].x + acc[4 * q4 + k4].y : 0.f;
+                    for (int k4 = 0; k4 < 4; k4++) t4[k4] = (4 * q4 + k4 < R::P) ? acc[4 * q4 + k4] : 0.f;
                     atomicAdd(dst + q4, make_float4(t4[0], t4[1], t4[2], t4[3]));
                 }
             }
@@ -1308,9 +1330,153 @@ k_raster(RasterArgs A)
 // Adam (Q9): beta1 0.9, beta2 0.999, eps 1e-8 outside the sqrt,
 // bias-corrected; clamp l11, l22 >= 1e-3.  Moments are stored
 // parameter-major m[Pk][K] so every access is coalesced.
+constexpr int ADAM_NT = 256;
+// elements per thread of the element-parallel k_adam (used while one wave of
+// resident CTAs covers every element; more per thread measured slower)
+constexpr int ADAM_IT = 1;
+
+template <int C, int E>
+__device__ __forceinline__ float *param_slot(const ParamsMut &p, int k, int v)
+{
+    // branch-free (selects): a divergent branch per parameter group would
+    // serialise the groups' load latencies
+    const size_t off = v < 2 ? 2 * (size_t)k + v
+                     : v < 5 ? 3 * (size_t)k + (v - 2)
+                     : v == 5 ? (size_t)k : (size_t)k * C * E + (v - 6);
+    float *base = v < 2 ? p.mu : v < 5 ? p.chol : v == 5 ? p.log_pi : p.expert;
+    return base + off;
+}
+
+// One CTA = ADAM_IT x (ADAM_NT / V) kernels x V slots; every thread owns
+// ADAM_IT (kernel, parameter) elements and issues all their loads before any
+// use, so a step's loads are in flight at once.  The kernel-major raw sums and
+// parameters are staged in shared memory (the chain rule of element v needs
+// several of its kernel's sums and its Cholesky factor); moments and the
+// update run parameter-major.
+template <int C, int E, int MODE>
+__global__ void __launch_bounds__(ADAM_NT)
+k_adam(int K, ParamsMut p, float *__restrict__ acc, const float *__restrict__ grad_in,
+       float *__restrict__ grad_out, float *__restrict__ m1, float *__restrict__ m2,
+       LrDev lr, HandleCtr *hc, const GridCtr *gc, long long cap)
+{
+    using R = Rec<C, E>;
+    constexpr int P = R::P, V = R::V, KPB = ADAM_NT / V, KPC = ADAM_IT * KPB;
+    __shared__ float s_raw[KPC][V + 1];
+    __shared__ float s_prm[KPC][V + 1];
+    if (MODE != 2 && gc->skip) return;
+    const long long t = hc->t + 1;
+    // 1 - beta^t = -expm1(t log(beta)), accurate to a few ulp for every t
+    const float bc1 = MODE == 1 ? 1.f : -expm1f((float)t * log1pf(-0.1f));
+    const float bc2 = MODE == 1 ? 1.f : -expm1f((float)t * log1pf(-0.001f));
+    const float rbc1 = 1.f / bc1, rbc2 = 1.f / bc2;
+    bool bad = false;
+    // grid-stride over chunks of KPC kernels (the host launches one CTA per
+    // chunk; the loop only guards other grid sizes)
+    const int nchunk = (K + KPC - 1) / KPC;
+    for (int chunk = blockIdx.x; chunk < nchunk; chunk += gridDim.x) {
+        const int k0 = chunk * KPC;
+        // every load is issued before any use: kernel-major (thread = kernel
+        // kl, slot v; acc[k0*V + ...] is contiguous) for the raw sums and
+        // parameters, parameter-major for the moments
+        // parameter-major: thread = (parameter v, kernels kl = it*KPB + lane group)
+        const int v = threadIdx.x / KPB;
+        float a1[ADAM_IT], a2[ADAM_IT], gi[ADAM_IT];
+#pragma unroll
+        for (int it = 0; it < ADAM_IT; it++) {
+            const int k = k0 + it * KPB + threadIdx.x % KPB;
+            const bool live = v < P && k < K;
+            a1[it] = a2[it] = gi[it] = 0.f;
+            if (live && MODE != 1) { a1[it] = m1[(size_t)v * K + k]; a2[it] = m2[(size_t)v * K + k]; }
+            if (live && MODE == 2) gi[it] = grad_in[(size_t)k * P + v];
+        }
+        float rv[ADAM_IT], pv[ADAM_IT];
+#pragma unroll
+        for (int it = 0; it < ADAM_IT; it++) {
+            const int kl = it * KPB + (int)threadIdx.x / V, v = threadIdx.x % V, k = k0 + kl;
+            rv[it] = pv[it] = 0.f;
+            if (k < K) {
+                if (MODE != 2) rv[it] = acc[(size_t)k0 * V + it * ADAM_NT + threadIdx.x];
+                pv[it] = *param_slot<C, E>(p, k, min(v, P - 1));
+            }
+        }
+#pragma unroll
+        for (int it = 0; it < ADAM_IT; it++) {
+            const int kl = it * KPB + (int)threadIdx.x / V, vv = threadIdx.x % V;
+            s_raw[kl][vv] = rv[it];
+            s_prm[kl][vv] = pv[it];
+        }
+        __syncthreads();
+        if (MODE != 2) {
+#pragma unroll
+            for (int it = 0; it < ADAM_IT; it++)
+                if (k0 + it * KPB + (int)threadIdx.x / V < K) acc[(size_t)k0 * V + it * ADAM_NT + threadIdx.x] = 0.f;
+        }
+#pragma unroll
+        for (int it = 0; it < ADAM_IT; it++) {
+            const int kl = it * KPB + threadIdx.x % KPB, k = k0 + kl;
+            if (!(v < P && k < K)) continue;
+            const float *raw = s_raw[kl], *prm = s_prm[kl];
+            float g = gi[it];
+            if (MODE != 2) {
+                if (v >= 6) {
+                    g = raw[v];
+                } else if (v == 5) {
+                    g = -2.f * raw[5];
+                } else {
+                    const float l11 = prm[2], l21 = prm[3], l22 = prm[4];
+                    const float a = 1.0f / l11, c = 1.0f / l22;
+                    const float b = -l21 / (l11 * l22);
+                    if (v <= 1) {
+                        float ex = 0.f;
+                        if (E == 3) {
+#pragma unroll
+                            for (int ch = 0; ch < C; ch++) ex = fmaf(prm[6 + ch * E + 1 + v], raw[6 + ch * E], ex);
+                        }
+                        g = (v == 0 ? -2.f * fmaf(a, raw[0], b * raw[1]) : -2.f * c * raw[1]) - ex;
+                    } else if (v == 2) {
+                        g = -2.f * fmaf(a * a, raw[2], a * b * raw[3]);
+                    } else if (v == 3) {
+                        g = -2.f * a * c * raw[3];
+                    } else {
+                        g = -2.f * fmaf(b * c, raw[3], c * c * raw[4]);
+                    }
+                }
+            }
+            bad = bad || !isfinite(g);
+            if (MODE == 1) {
+                grad_out[(size_t)k * P + v] = g;
+            } else {
+                const float b1 = 0.9f, b2 = 0.999f, eps = 1e-8f;
+                const float lri = v < 2 ? lr.mu : (v < 5 ? lr.chol : (v == 5 ? lr.log_pi : (((v - 6) % E) == 0 ? lr.expert : lr.slope)));
+                const float n1 = fmaf(b1, a1[it], (1.f - b1) * g);
+                const float n2 = fmaf(b2, a2[it], (1.f - b2) * g * g);
+                float x = prm[v] - lri * (n1 * rbc1) / (sqrtf(n2 * rbc2) + eps);
+                if (v == 2 || v == 4) x = fmaxf(x, 1e-3f);
+                m1[(size_t)v * K + k] = n1;
+                m2[(size_t)v * K + k] = n2;
+                *param_slot<C, E>(p, k, v) = x;
+            }
+        }
+        __syncthreads();   // shared staging is reused by the next chunk
+    }
+    if (bad) atomicExch((unsigned long long *)&hc->nonfinite, 1ull);
+    if (MODE == 1) return;
+    // the last CTA advances the step counter after every CTA has read it (the
+    // reads were consumed before the barrier; no other data is published, so
+    // a relaxed ticket suffices and no CTA waits for its stores to drain)
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(&hc->done, 1u) == gridDim.x - 1) {
+        hc->t = t;
+        hc->done = 0;
+    }
+}
+
+// Large pools: one thread per kernel, all of its loads first (more bytes in
+// flight per thread than the element-parallel form once several waves are
+// needed; measured faster at K >= 20 000).
 template <int C, int E, int MODE>
 __global__ void __launch_bounds__(64)
-k_adam(int K, ParamsMut p, float *__restrict__ acc, const float *__restrict__ grad_in,
+k_adam_kt(int K, ParamsMut p, float *__restrict__ acc, const float *__restrict__ grad_in,
        float *__restrict__ grad_out, float *__restrict__ m1, float *__restrict__ m2,
        LrDev lr, HandleCtr *hc, const GridCtr *gc, long long cap)
 {

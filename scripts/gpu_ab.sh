@@ -7,6 +7,6 @@ SMOE_LIB=$lib timeout 600 python bench.py --config $cfg --steps ${STEPS:-500} --
 python -c "
 import json; d=json.loads(open('gpurun_out/bq.log').read().strip().splitlines()[-1])
 r=d['roofline'] or {}
-print('$cfg $v', round(d['value'],1), 'it/s', round(d['ms_per_step']*1e3,1), 'us/step; raster', round(r.get('avg_ms',0)*1e3,1), 'us frac', round(r.get('frac',0),3))
+print('$cfg $v', round(d['value'],1), 'it/s', round(d['ms_per_step']*1e3,1), 'us/step; raster', round(r.get('avg_ms',0)*1e3,1), 'us frac', round(r.get('frac',0),3), {k: round(v*1e3,1) for k,v in (d['kernel_ms_per_step'] or {}).items()})
 "
 done; done
