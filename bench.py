@@ -234,6 +234,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--K", type=int, default=0, help="override the config's kernel count (density sweeps; not a bench line)")
     ap.add_argument("--backward-mode", type=int, default=-1, help="-1 auto (default), 0 pixel-parallel, 1 kernel-parallel")
     ap.add_argument("--no-profile", action="store_true", help="no per-kernel events in the timed region")
     ap.add_argument("--seg", type=float, default=0.0,
@@ -257,9 +258,11 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = synth.CONFIGS[args.config]
+    cfg = dict(synth.CONFIGS[args.config])
+    if args.K > 0:
+        cfg["K"] = args.K
     C, H, W, K, order = cfg["C"], cfg["H"], cfg["W"], cfg["K"], cfg["order"]
-    target, _, pool = synth.workload(args.config)
+    target, _, pool = synth.workload(args.config, args.K)
     dev = torch.device("cuda", local)
     tgt = torch.as_tensor(target).to(dev)
     params = smoe.Params.from_numpy(pool, dev)
@@ -440,7 +443,7 @@ def main():
             "metric": "SMoE fit iterations/s", "value": value, "unit": "it/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": config_dict(args.config, world),
+            "config": dict(config_dict(args.config, world), **({"K": K, "K_override": True} if args.K else {})),
             "render": render, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk,
             "kernel_ms_per_step": breakdown,

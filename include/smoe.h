@@ -97,10 +97,10 @@ typedef struct {
     double R2;                     /* truncation radius^2; default 2 ln 100 (Q1) */
     int device;                    /* CUDA device ordinal, -1 = current device   */
     long long pair_capacity;       /* initial pair capacity, 0 = automatic        */
-    int backward_mode;             /* -1 = auto (default: kernel-parallel unless
-                                      blocks average > 110 kernels), 0 = pixel-
-                                      parallel with warp reductions, 1 = kernel-
-                                      parallel over per-warp pair lists (§5)   */
+    int backward_mode;             /* -1 = auto (default: kernel-parallel), 0 =
+                                      pixel-parallel with warp reductions, 1 =
+                                      kernel-parallel over per-warp pixel-pair
+                                      lists                     */
     int use_graphs;                /* 1 (default): smoe_step / smoe_grad replay
                                       their launch sequence as a CUDA graph     */
     int head;                      /* regression head: 0 = SMoE soft gates

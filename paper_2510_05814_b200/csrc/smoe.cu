@@ -324,16 +324,14 @@ void read_ctl(smoe_ctx *h)
     if (h->h_ctl->train.pairs > 0) h->last_pairs = (double)h->h_ctl->train.pairs;
 }
 
-// Backward form: the kernel-parallel pass over per-warp pair
-// lists wins while blocks are sparse; with long lists (denser than ~110
-// kernels per block on average, e.g. config 4) the pixel-parallel pass with
-// warp reductions is faster.  Auto mode decides from the last observed P.
+// Backward form: the kernel-parallel pass over per-warp
+// pixel-pair lists, unless the caller forces the pixel-parallel pass with
+// warp reductions (smoe_options.backward_mode = 0).
 int effective_bwd(smoe_ctx *h)
 {
-    if (h->bwd_mode >= 0) return h->bwd_mode;
-    double nt = (double)((h->H + TILE - 1) / TILE) * ((h->W + TILE - 1) / TILE);
-    if (h->last_pairs < 0) return 1;
-    return h->last_pairs / nt > 110.0 ? 0 : 1;
+    // auto: kernel-parallel (measured faster at 23-604 kernels per block,
+    // configs 1-5 and a config-4 density sweep; scripts/gpu_density.sh)
+    return h->bwd_mode >= 0 ? h->bwd_mode : 1;
 }
 
 #define DISPATCH_CE(h, BODY)                                                  \

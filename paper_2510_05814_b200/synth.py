@@ -135,9 +135,12 @@ CONFIGS = {
 }
 
 
-def workload(name: str):
-    """(target, clean_image_or_None, pool) for a named BASELINE.json config."""
-    c = CONFIGS[name]
+def workload(name: str, K: int = 0):
+    """(target, clean_image_or_None, pool) for a named BASELINE.json config
+    (K > 0 overrides the kernel count: density sweeps)."""
+    c = dict(CONFIGS[name])
+    if K > 0:
+        c["K"] = K
     s = 1234 + c["cfg"]
     img = image(c["H"], c["W"], c["C"], s)
     target = noisy(img, c["noise"], s + 2) if "noise" in c else img
