@@ -104,9 +104,10 @@ struct Grid {
     int *chunk = nullptr, *hist = nullptr;    // fused binning scratch
     int bin_grid = 0;                         // cooperative grid of k_bin
     bool order_valid = false;                 // LPT order written by the last binning
-    // direct buckets (grids up to SCAN_SINGLE_MAX blocks): block t's list is
+    // direct buckets (grids up to DIRECT_MAX blocks): block t's list is
     // ids[t bcap, t bcap + len[t]); otherwise CSR lists ids[start[t], start[t+1])
     bool direct = false;
+    bool no_direct = false;   // calibration found the buckets too unbalanced for direct
     int bcap = 0;
     int *len = nullptr;
     long long cap = 0;
@@ -262,6 +263,10 @@ float *stage(float *&buf, size_t &have, size_t n)
     return buf;
 }
 
+// Direct buckets up to this many blocks (measured at 129 600 and 172 890:
+// config 5 preprocess 200 -> 132 us, config 3 4x render +11% over CSR lists)
+constexpr long long DIRECT_MAX = 1 << 18;
+
 void ensure_grid(smoe_ctx *h, Grid &g, GridCtr *gc, int oH, int oW)
 {
     if (g.oH == oH && g.oW == oW && g.cnt) return;
@@ -276,7 +281,9 @@ void ensure_grid(smoe_ctx *h, Grid &g, GridCtr *gc, int oH, int oW)
     g.gc = gc;
     {
         const char *e = getenv("SMOE_CSR");
-        bool direct = g.n_tiles <= SCAN_SINGLE_MAX && !(e && atoi(e) != 0);
+        const char *dm = getenv("SMOE_DIRECT_MAX");
+        const long long direct_max = dm ? atoll(dm) : DIRECT_MAX;
+        bool direct = g.n_tiles <= direct_max && !g.no_direct && !(e && atoi(e) != 0);
         if (direct != g.direct) { dfree(g.ids); dfree(g.tmp); cap = 0; cal = false; g.bcap = 0; }
         g.direct = direct;
         if (direct) {
@@ -369,7 +376,7 @@ void bin_unfused(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_h
     int K = h->K;
     int nb = (K + PRE_NT - 1) / PRE_NT;
     float sx = (float)g.oW / (float)h->W, sy = (float)g.oH / (float)h->H;
-    if (g.n_tiles > SCAN_SINGLE_MAX && !g.lb_state) {
+    if (!g.direct && g.n_tiles > SCAN_SINGLE_MAX && !g.lb_state) {
         size_t nbl = (g.n_tiles + LB_CHUNK - 1) / LB_CHUNK;
         CK(cudaMalloc(&g.lb_state, sizeof(unsigned long long) * nbl));
         CK(cudaMemsetAsync(g.lb_state, 0, sizeof(unsigned long long) * nbl, h->stream));
@@ -389,10 +396,20 @@ void bin_unfused(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_h
             CK(cudaMemcpyAsync(cn, &g.gc->pairs, sizeof(cn), cudaMemcpyDeviceToHost, h->stream));
             CK(cudaStreamSynchronize(h->stream));
             if (&g == &h->train) h->last_pairs = (double)cn[0];
+            // no raster consumed this binning: reset its counts
+            CK(cudaMemsetAsync(g.cnt, 0, sizeof(int) * g.n_tiles, h->stream));
+            if (g.n_tiles > SCAN_SINGLE_MAX && cn[1] * (long long)g.n_tiles > 8 * cn[0] + (1ll << 24)) {
+                // fixed-capacity buckets would be mostly empty: CSR lists instead
+                g.no_direct = true;
+                const int oH = g.oH, oW = g.oW;
+                g.oH = 0;
+                ensure_grid(h, g, g.gc, oH, oW);
+                return bin_unfused(h, g, p, ty_lo, ty_hi, zero_stats, lscale);
+            }
             grow(h, g, cn[1] > 0 ? cn[1] : 1);
             return bin_unfused(h, g, p, ty_lo, ty_hi, zero_stats, lscale);
         }
-        g.order_valid = use_lpt(g);
+        g.order_valid = false;   // direct buckets: identity block order
         return;
     }
     if (g.lb_state) {
@@ -525,7 +542,7 @@ void forward_backward(smoe_ctx *h, const smoe_params *p, const float *target)
     if (nt <= 0) return;
     RasterArgs A{};
     A.rec = h->rec; A.ids = g.ids; A.tmp = g.tmp; A.start = g.start; A.gc = g.gc; A.cap = g.cap;
-    A.len = g.direct ? g.len : nullptr; A.bcap = g.bcap;
+    A.len = g.direct ? g.cnt : nullptr; A.lenout = g.len; A.bcap = g.bcap;
     A.order = g.order_valid ? g.order : nullptr;
     A.gcw = g.gc; A.n_work = nt; A.n_sm = h->n_sm;
     A.nx = g.nx; A.tile0 = ty_lo * g.nx; A.oW = h->W; A.oH = h->H;
@@ -1068,7 +1085,7 @@ smoe_status smoe_render_ex(smoe_handle h, const smoe_params *p, int out_H, int o
             float *o = odev ? out : stage(h->stage_out, h->stage_out_n, n);
             RasterArgs A{};
             A.rec = h->rec; A.ids = g.ids; A.tmp = g.tmp; A.start = g.start; A.gc = g.gc; A.cap = g.cap;
-            A.len = g.direct ? g.len : nullptr; A.bcap = g.bcap;
+            A.len = g.direct ? g.cnt : nullptr; A.lenout = g.len; A.bcap = g.bcap;
             A.order = g.order_valid ? g.order : nullptr; A.gcw = g.gc; A.n_work = g.n_tiles; A.n_sm = h->n_sm;
             A.nx = g.nx; A.tile0 = 0; A.oW = out_W; A.oH = out_H;
             A.sx = (float)h->W / (float)out_W; A.sy = (float)h->H / (float)out_H;

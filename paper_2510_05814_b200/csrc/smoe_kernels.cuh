@@ -58,6 +58,9 @@ struct GridCtr {
     unsigned int scan_done;  // k_scan_lookback: finished-CTA ticket
     unsigned int epoch;      // k_scan_lookback: tag of the current scan
     unsigned int skip;       // 1: the last binning overflowed its capacity (consumers skip)
+    unsigned long long acc_pairs;  // direct buckets: pairs emitted by this binning (CTA sums)
+    int acc_max;             // direct buckets: longest bucket of this binning
+    int pad2;
 };
 
 // Per-handle device counters.
@@ -188,7 +191,8 @@ __device__ __forceinline__ void
 preprocess_one(int k, ParamsDev p, float R2, float sx, float sy, int oW, int oH,
                int nx, int ty_lo, int ty_hi, float *__restrict__ rec,
                int4 *__restrict__ tbox, int *__restrict__ cnt, HandleCtr *hc, float lscale,
-               bool direct = false, int *__restrict__ dids = nullptr, int bcap = 0)
+               bool direct = false, int *__restrict__ dids = nullptr, int bcap = 0,
+               int *n_emit = nullptr, int *max_len = nullptr)
 {
     using R = Rec<C, E>;
     float2 mu = reinterpret_cast<const float2 *>(p.mu)[k];
@@ -239,9 +243,12 @@ preprocess_one(int k, ParamsDev p, float R2, float sx, float sy, int oW, int oH,
                     sl[q] = i < nbx ? atomicAdd(&cnt[t[q]], 1) : bcap;
                 }
 #pragma unroll
-                for (int q = 0; q < 4; q++)
+                for (int q = 0; q < 4; q++) {
                     if (sl[q] < bcap) dids[(size_t)t[q] * bcap + sl[q]] = k;
+                    if (i0 + q < nbx) *max_len = max(*max_len, sl[q] + 1);
+                }
             }
+            *n_emit = nbx;
         } else {
             for (int ty = y0; ty <= y1; ty++)
                 for (int tx = tb.x; tx <= tb.y; tx++) atomicAdd(&cnt[ty * nx + tx], 1);
@@ -252,85 +259,28 @@ preprocess_one(int k, ParamsDev p, float R2, float sx, float sy, int oW, int oH,
 
 constexpr int PRE_NT = 256;
 
-// Direct buckets (a1 + a3 in one pass, small grids): kernel k's id went
-// straight into the slot its count atomic returned in block t's fixed-capacity
-// bucket ids[t * bcap, ...).  The last CTA of k_preprocess publishes the
-// bucket lengths (len), P and the largest bucket, latches overflow (a bucket
-// longer than bcap: consumers skip, the host regrows), zeroes the counts and
-// the loss partials, and builds the LPT order of the band's blocks.
-__device__ __forceinline__ void finish_direct(int *__restrict__ cnt, int n, int *__restrict__ len, int bcap,
-                                              GridCtr *gc, double *dstats, int *__restrict__ order, int t0,
-                                              int nt)
+// Direct buckets (a1 + a3 in one pass): kernel k's id went straight into the
+// slot its count atomic returned in block t's fixed-capacity bucket
+// ids[t * bcap, ...).  The count array is the bucket-length array: the
+// raster CTA of block t reads it and resets it (no pass over the blocks
+// here).  Every CTA adds its pair count and longest slot to the grid
+// counters; the last CTA of k_preprocess publishes P, latches overflow (a
+// bucket longer than bcap: consumers skip, the host regrows), and zeroes the
+// loss partials.
+__device__ __forceinline__ void finish_direct(int bcap, GridCtr *gc, double *dstats)
 {
-    __shared__ unsigned long long sP;
-    __shared__ int sMax;
-    __shared__ int hist[256];
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    if (tid == 0) { sP = 0ull; sMax = 0; }
-    if (tid < 4 && dstats) dstats[tid] = 0.0;
-    hist[tid] = 0;
-    __syncthreads();
-    unsigned long long p = 0;
-    int mx = 0;
-    constexpr int U = 8;   // counts in flight per thread
-    for (int base = tid; base < n; base += U * PRE_NT) {
-        int c[U];
-#pragma unroll
-        for (int q = 0; q < U; q++) c[q] = base + q * PRE_NT < n ? __ldcg(cnt + base + q * PRE_NT) : 0;
-#pragma unroll
-        for (int q = 0; q < U; q++) {
-            const int i = base + q * PRE_NT;
-            if (i < n) {
-                len[i] = c[q];
-                cnt[i] = 0;
-                p += (unsigned)c[q];
-                mx = max(mx, c[q]);
-                if (order && i >= t0 && i < t0 + nt) atomicAdd(&hist[255 - min(c[q], 255)], 1);
-            }
-        }
-    }
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-        p += __shfl_xor_sync(FULL, p, o);
-        mx = max(mx, __shfl_xor_sync(FULL, mx, o));
-    }
-    if (lane == 0) { atomicAdd(&sP, p); atomicMax(&sMax, mx); }
-    __syncthreads();
-    if (tid == 0) {
-        const long long P = (long long)sP;
+    if (threadIdx.x < 4 && dstats) dstats[threadIdx.x] = 0.0;
+    if (threadIdx.x == 0) {
+        const long long P = (long long)__ldcg(&gc->acc_pairs);
+        const int mx = __ldcg(&gc->acc_max);
+        gc->acc_pairs = 0ull;
+        gc->acc_max = 0;
         gc->pairs = P;
-        const bool ovf = sMax > bcap;
+        const bool ovf = mx > bcap;
         gc->skip = ovf ? 1u : 0u;
         if (ovf) {
-            if (sMax > gc->need) gc->need = sMax;
+            if (mx > gc->need) gc->need = mx;
             gc->skipped += 1;
-        }
-    }
-    if (!order) return;
-    {
-        int v = hist[tid], inc = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int t = __shfl_up_sync(FULL, inc, o);
-            if (lane >= o) inc += t;
-        }
-        __shared__ int wt[PRE_NT / 32];
-        if (lane == 31) wt[wid] = inc;
-        __syncthreads();
-        int pre = 0;
-        for (int w = 0; w < wid; w++) pre += wt[w];
-        __syncthreads();
-        hist[tid] = pre + inc - v;
-    }
-    __syncthreads();
-    for (int base = tid; base < n; base += U * PRE_NT) {
-        int c[U];
-#pragma unroll
-        for (int q = 0; q < U; q++) c[q] = base + q * PRE_NT < n ? len[base + q * PRE_NT] : 0;   // own writes
-#pragma unroll
-        for (int q = 0; q < U; q++) {
-            const int i = base + q * PRE_NT;
-            if (i < n && i >= t0 && i < t0 + nt) order[atomicAdd(&hist[255 - min(c[q], 255)], 1)] = i;
         }
     }
 }
@@ -345,21 +295,43 @@ k_preprocess(int K, ParamsDev p, float R2, float sx /* oW/W */, float sy /* oH/H
              int *__restrict__ dids, int bcap, int *__restrict__ len)
 {
     int k = blockIdx.x * blockDim.x + threadIdx.x;
+    int n_emit = 0, max_len = 0;
     if (k < K)
         preprocess_one<C, E>(k, p, R2, sx, sy, oW, oH, nx, ty_lo, ty_hi, rec, tbox, cnt, hc, lscale, len != nullptr,
-                             dids, bcap);
-    if (!order) return;   // large grid: k_scan_lookback follows
-    // the last CTA to finish scans the counts (a2)
+                             dids, bcap, &n_emit, &max_len);
+    if (len) {
+        // direct buckets: this CTA's pairs and longest slot to the grid counters
+        __shared__ unsigned long long s_pairs;
+        __shared__ int s_max;
+        if (threadIdx.x == 0) { s_pairs = 0ull; s_max = 0; }
+        __syncthreads();
+        unsigned long long pe = (unsigned)n_emit;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            pe += __shfl_xor_sync(FULL, pe, o);
+            max_len = max(max_len, __shfl_xor_sync(FULL, max_len, o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            if (pe) atomicAdd(&s_pairs, pe);
+            if (max_len) atomicMax(&s_max, max_len);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            if (s_pairs) atomicAdd(&gc->acc_pairs, s_pairs);
+            if (s_max) atomicMax(&gc->acc_max, s_max);
+        }
+    }
+    if (!order && !len) return;   // large grid: k_scan_lookback follows
+    // the last CTA to finish publishes the grid's totals (a2)
     // (grid-sync pattern: barrier, then one acq_rel ticket by thread 0; the
-    // last CTA reads the counts from L2)
+    // last CTA reads the counters from L2)
     __shared__ bool last;
     __syncthreads();
     if (threadIdx.x == 0) last = atom_add_acq_rel_gpu(&gc->ticket, 1u) == gridDim.x - 1;
     __syncthreads();
     if (!last) return;
     if (len) {
-        finish_direct(cnt, n_tiles, len, bcap, gc, dstats, build_order ? order : nullptr, ty_lo * nx,
-                      (ty_hi - ty_lo) * nx);
+        finish_direct(bcap, gc, dstats);
         if (threadIdx.x == 0) { gc->ticket = 0; gc->work = 0; }
         return;
     }
@@ -851,7 +823,9 @@ struct RasterArgs {
     int *ids;             // block lists (bucket-sorted in place by the raster)
     int *tmp;             // merge scratch for buckets larger than the smem chunk
     const int *start;     // CSR lists: block t = ids[start[t], start[t+1])
-    const int *len;       // direct buckets (len != null): block t = ids[t bcap, t bcap + len[t])
+    int *len;             // direct buckets (len != null): block t = ids[t bcap, t bcap + len[t]);
+                          // len = the binning's count array, reset by the block's CTA
+    int *lenout;          // direct buckets: copy of len for the diagnostics (smoe_bin)
     int bcap;
     const GridCtr *gc;
     long long cap;
@@ -948,6 +922,15 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
     const float R2 = A.R2;
     const int s0 = A.len ? tile * A.bcap : A.start[tile];
     const int n = A.len ? A.len[tile] : A.start[tile + 1] - s0;
+    // direct buckets: the count is consumed here and reset for the next
+    // binning (when n > 0 every thread has read it before thread 0 passes the
+    // first batch barrier, and thread 0 resets it only at its return)
+    auto release = [&] {
+        if (A.len && threadIdx.x == 0) {
+            A.lenout[tile] = n;
+            if (n) A.len[tile] = 0;
+        }
+    };
     // a4 (second digit): sort this block's bucket by kernel id; srec doubles
     // as the shared scratch (its capacity in ints is a power of two >= 1024)
     constexpr int SCHUNK = (BATCH * RS4 * 4 >= 2048) ? 2048 : 1024;
@@ -1058,6 +1041,7 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
                 if (v1) o1[c * plane] = y1[c];
             }
         }
+        release();
         return;
     }
 
@@ -1158,6 +1142,7 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
                     atomicAdd(&A.acc[(size_t)sid[j] * R::V + idx], tot);
             }
         }
+        release();
         return;
     }
 
@@ -1298,6 +1283,7 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
         }
         __syncthreads();
     }
+    release();
 }
 
 // Raster grid: one CTA per block.  CTAs take the blocks in the LPT order
@@ -1309,11 +1295,15 @@ template <int C, int E, bool TRAIN, bool PROF, bool KPAR>
 __global__ void __launch_bounds__(128, KPAR ? (E == 3 ? SMOE_KPAR_MINB : SMOE_KPAR_MINB_CONST) : 12)
 k_raster(RasterArgs A)
 {
-    if (A.gc->skip) return;
     int i = blockIdx.x;
     const int k = i / A.n_sm, j = i - k * A.n_sm;
     if ((k & 1) && (k + 1) * A.n_sm <= A.n_work) i = k * A.n_sm + (A.n_sm - 1 - j);
-    raster_tile<C, E, TRAIN, PROF, KPAR>(A, A.order ? A.order[i] : A.tile0 + i);
+    const int tile = A.order ? A.order[i] : A.tile0 + i;
+    if (A.gc->skip) {   // overflowed binning: no work, but the counts are reset
+        if (A.len && threadIdx.x == 0) A.len[tile] = 0;
+        return;
+    }
+    raster_tile<C, E, TRAIN, PROF, KPAR>(A, tile);
 }
 
 // ---------------------------------------------------------------- a8 ------

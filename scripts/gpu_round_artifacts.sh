@@ -5,6 +5,7 @@ mkdir -p gpurun_out/art
 TAG=${TAG:-r01}
 O=gpurun_out/art
 python -c "import __graft_entry__ as g; g.smoke()" > $O/${TAG}_smoke.log 2>&1; echo smoke=$?
+timeout 900 python -m pytest tests -m gpu -q > $O/${TAG}_pytest_gpu.log 2>&1; echo pytest=$?; tail -1 $O/${TAG}_pytest_gpu.log
 timeout 900 python bench.py > $O/${TAG}_bench_default.log 2>&1; echo bench=$?; tail -1 $O/${TAG}_bench_default.log | cut -c1-300
 timeout 900 python bench.py --impl reference --steps 20 --warmup 3 > $O/${TAG}_bench_reference.log 2>&1; echo ref=$?
 for cfg in tiny denoise div2k 8k; do
@@ -24,11 +25,15 @@ timeout 1200 compute-sanitizer --tool $tool --print-limit 20 --error-exitcode 7 
    -k "test_grad_parity and 37 or test_render_parity and 37 or binning_large_bucket or dense_buckets or degenerate or step_matches or capacity" > $O/${TAG}_sanitizer_$tool.txt 2>&1
 echo $tool=$?; tail -2 $O/${TAG}_sanitizer_$tool.txt
 done
-for CFG in kodak 8k; do
+for CFG in ${NCU_CFGS:-kodak div2k denoise 8k}; do
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${TAG}_launches_${CFG}_final.csv \
     python bench.py --config $CFG --steps 30 --warmup 3 --no-cpu --no-e2e --no-profile > /dev/null 2>&1
 echo launches_$CFG=$?
 ncu --set full --clock-control none --import-source on -k regex:'^k_' -s 20 -c 4 -f -o $O/prof_${CFG} \
     python bench.py --config $CFG --steps 10 --warmup 5 --no-cpu --no-e2e --no-profile > /dev/null 2>&1
 echo full_$CFG=$?
+# summaries on the box (the reports are too large to bring back; kodak's is kept)
+SMOE_PROFILES_DIR=$O/profiles python scripts/ncu_summary.py ${TAG}_ncu_${CFG}_final $CFG $O/${TAG}_launches_${CFG}_final.csv $O/prof_${CFG}.ncu-rep > /dev/null 2>&1; echo summary_$CFG=$?
+[ $CFG = kodak ] || rm -f $O/prof_${CFG}.ncu-rep
 done
+du -sh $O

@@ -80,9 +80,13 @@ def main():
     ours = {k: v for k, v in ll.items() if k.startswith("k_")}
     tot = sum(v["mean_us"] * v["n"] for v in ours.values())
     res["share_of_library_time"] = {k: v["mean_us"] * v["n"] / tot for k, v in ours.items()}
-    os.makedirs(os.path.join(root, "profiles"), exist_ok=True)
-    json.dump(res, open(os.path.join(root, "profiles", f"{tag}.json"), "w"), indent=1)
-    tpath = os.path.join(root, "profiles", "ncu_raster_traffic.json")
+    pdir = os.environ.get("SMOE_PROFILES_DIR", os.path.join(root, "profiles"))
+    os.makedirs(pdir, exist_ok=True)
+    json.dump(res, open(os.path.join(pdir, f"{tag}.json"), "w"), indent=1)
+    tpath = os.path.join(pdir, "ncu_raster_traffic.json")
+    if not os.path.exists(tpath) and os.path.exists(os.path.join(root, "profiles", "ncu_raster_traffic.json")):
+        import shutil
+        shutil.copy(os.path.join(root, "profiles", "ncu_raster_traffic.json"), tpath)
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
     for k, d in res["full_capture"].items():
         if k.startswith("k_raster") and k.endswith(", 1, 1>") or (k.startswith("k_raster") and ", 1," in k):

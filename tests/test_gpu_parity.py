@@ -111,10 +111,14 @@ def test_binning_large_bucket_merge_path():
     np.testing.assert_array_equal(ids.numpy(), ids_ref)
 
 
-def test_large_grid_lookback_scan_and_render():
-    """An output raster with more than 32768 blocks takes the multi-CTA
-    look-back scan (and the identity block order); lists stay bit-exact and
-    sampled pixels match the oracle."""
+@pytest.mark.parametrize("direct_max", ["", "32768"])
+def test_large_grid_lookback_scan_and_render(direct_max, monkeypatch):
+    """An output raster with more than 32768 blocks: direct buckets (default)
+    or, with direct buckets capped at 32768 blocks, CSR lists built by the
+    multi-CTA look-back scan; lists stay bit-exact and sampled pixels match
+    the oracle."""
+    if direct_max:
+        monkeypatch.setenv("SMOE_DIRECT_MAX", direct_max)
     H, W, C, K = 1456, 1456, 3, 300
     oH = oW = 2912                       # 182 x 182 = 33124 blocks
     pool = synth.aniso_pool(H, W, C, K, 61, order=1, margin_px=4)
@@ -666,3 +670,24 @@ def test_checkpoint_resume():
     d_resume = (saved.flat() - pa.flat()).abs().max().item()
     d_fresh = (fresh.flat() - pa.flat()).abs().max().item()
     assert d_resume < 1e-4 and d_fresh > 100 * d_resume, (d_resume, d_fresh)
+
+
+def test_large_grid_unbalanced_buckets_fall_back_to_csr():
+    """33124 blocks with every kernel inside one block: fixed-capacity buckets
+    would be almost all empty, so the calibration switches the grid to CSR
+    lists; lists stay bit-exact and a training step works."""
+    H = W = 2912                         # 182 x 182 = 33124 blocks
+    K = 3000
+    g = np.random.default_rng(4)
+    pool = synth.aniso_pool(H, W, 1, K, 63, l_range=(0.3, 0.6), shear=0.1)
+    pool.mu[:] = g.uniform(1000.2, 1007.8, (K, 2)).astype(np.float32)
+    pool = conditioned(pool, H, W)
+    h = smoe.SMoE(K, H, W, 1, 0)
+    p = dev_pool(pool)
+    rng, ids, tb = h.bin(p, H, W)
+    _, tb_ref, _ = O.boxes(opar(pool), H, W)
+    rng_ref, ids_ref = O.tile_list(tb_ref, 182, 182)
+    np.testing.assert_array_equal(rng.numpy(), rng_ref)
+    np.testing.assert_array_equal(ids.numpy(), ids_ref)
+    st = h.step(p, torch.zeros(1, H, W, device="cuda"), smoe.LR())
+    assert np.isfinite(st.loss) and st.pairs == len(ids_ref)
