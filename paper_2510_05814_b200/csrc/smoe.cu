@@ -374,7 +374,11 @@ void check_params(const smoe_params *p)
 void bin_unfused(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_hi, bool zero_stats, float lscale)
 {
     int K = h->K;
-    int nb = (K + PRE_NT - 1) / PRE_NT;
+    // direct buckets need no CTA-wide block pass, so smaller CTAs spread the
+    // count atomics over more SMs
+    static const int pre_nt_direct = getenv("SMOE_PRE_NT_DIRECT") ? atoi(getenv("SMOE_PRE_NT_DIRECT")) : PRE_NT;
+    const int pre_nt = g.direct ? pre_nt_direct : PRE_NT;
+    int nb = (K + pre_nt - 1) / pre_nt;
     float sx = (float)g.oW / (float)h->W, sy = (float)g.oH / (float)h->H;
     if (!g.direct && g.n_tiles > SCAN_SINGLE_MAX && !g.lb_state) {
         size_t nbl = (g.n_tiles + LB_CHUNK - 1) / LB_CHUNK;
@@ -382,7 +386,7 @@ void bin_unfused(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_h
         CK(cudaMemsetAsync(g.lb_state, 0, sizeof(unsigned long long) * nbl, h->stream));
     }
     launch(h, SMOE_KERNEL_PREPROCESS, "k_preprocess", [&] {
-        DISPATCH_CE(h, (k_preprocess<C_, E_><<<nb, PRE_NT, 0, h->stream>>>(
+        DISPATCH_CE(h, (k_preprocess<C_, E_><<<nb, pre_nt, 0, h->stream>>>(
                            K, pdev(p), h->R2, sx, sy, g.oW, g.oH, g.nx, ty_lo, ty_hi, h->rec, h->tbox,
                            g.cnt, &h->ctl->hc, g.n_tiles, g.start, g.cursor, g.cap, g.gc,
                            zero_stats ? h->ctl->dstats : nullptr, g.lb_state ? nullptr : g.order, lscale,

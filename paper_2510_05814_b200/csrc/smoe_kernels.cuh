@@ -1196,46 +1196,46 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
             // one entry's contribution to the raw sums (a pixel outside the ellipse: g = 0)
             auto add_entry = [&](const unsigned e) {
                 const int l = (int)((e >> 2) & 31u);
-                    const float4 pa = spw_pix[2 * l], pb = spw_pix[2 * l + 1];
-                    const float dx = xw + (float)(l & 7) - r[0];
-                    const float yl = yw + (float)((l >> 3) * 2) - r[1];
-                    const float2 dy = make_float2(yl, yl + 1.0f);
-                    const float u = r[2] * dx;
-                    const float bdx = r[3] * dx;
-                    const float2 v = __ffma2_rn(make_float2(r[4], r[4]), dy, make_float2(bdx, bdx));
-                    const float uu = u * u;
-                    const float2 qd = __ffma2_rn(v, v, make_float2(uu, uu));
-                    const float2 ea = __ffma2_rn(qd, make_float2(-0.5f * LOG2E, -0.5f * LOG2E), make_float2(r[5], r[5]));
-                    const float2 g = make_float2((e & 1u) ? ex2_approx(ea.x) : 0.f, (e & 2u) ? ex2_approx(ea.y) : 0.f);
-                    const float2 eda[4] = {make_float2(pa.x, pa.y), make_float2(pa.z, pa.w),
-                                           make_float2(pb.x, pb.y), make_float2(pb.z, pb.w)};
-                    float2 Gs = make_float2(-eda[3].x, -eda[3].y);
-    #pragma unroll
-                    for (int c = 0; c < C; c++) {
-                        float2 mc = make_float2(r[6 + c * E], r[6 + c * E]);
-                        if (E == 3) {
-                            const float mb = fmaf(r[6 + c * E + 1], dx, r[6 + c * E]);
-                            mc = __ffma2_rn(make_float2(r[6 + c * E + 2], r[6 + c * E + 2]), dy, make_float2(mb, mb));
-                        }
-                        Gs = __ffma2_rn(eda[c], mc, Gs);
-                        const float2 ge = __fmul2_rn(g, eda[c]);
-                        const float gsum = ge.x + ge.y;
-                        acc[6 + c * E] += gsum;
-                        if (E == 3) {
-                            acc[6 + c * E + 1] = fmaf(gsum, dx, acc[6 + c * E + 1]);
-                            acc[6 + c * E + 2] = fmaf(ge.x, dy.x, fmaf(ge.y, dy.y, acc[6 + c * E + 2]));
-                        }
+                const float4 pa = spw_pix[2 * l], pb = spw_pix[2 * l + 1];
+                const float dx = xw + (float)(l & 7) - r[0];
+                const float yl = yw + (float)((l >> 3) * 2) - r[1];
+                const float2 dy = make_float2(yl, yl + 1.0f);
+                const float u = r[2] * dx;
+                const float bdx = r[3] * dx;
+                const float2 v = __ffma2_rn(make_float2(r[4], r[4]), dy, make_float2(bdx, bdx));
+                const float uu = u * u;
+                const float2 qd = __ffma2_rn(v, v, make_float2(uu, uu));
+                const float2 ea = __ffma2_rn(qd, make_float2(-0.5f * LOG2E, -0.5f * LOG2E), make_float2(r[5], r[5]));
+                const float2 g = make_float2((e & 1u) ? ex2_approx(ea.x) : 0.f, (e & 2u) ? ex2_approx(ea.y) : 0.f);
+                const float2 eda[4] = {make_float2(pa.x, pa.y), make_float2(pa.z, pa.w),
+                                       make_float2(pb.x, pb.y), make_float2(pb.z, pb.w)};
+                float2 Gs = make_float2(-eda[3].x, -eda[3].y);
+#pragma unroll
+                for (int c = 0; c < C; c++) {
+                    float2 mc = make_float2(r[6 + c * E], r[6 + c * E]);
+                    if (E == 3) {
+                        const float mb = fmaf(r[6 + c * E + 1], dx, r[6 + c * E]);
+                        mc = __ffma2_rn(make_float2(r[6 + c * E + 2], r[6 + c * E + 2]), dy, make_float2(mb, mb));
                     }
-                    const float2 sg = __fmul2_rn(__fmul2_rn(make_float2(-0.5f, -0.5f), g), Gs);
-                    const float ssum = sg.x + sg.y;
-                    const float2 sv = __fmul2_rn(sg, v);
-                    const float svsum = sv.x + sv.y;
-                    acc[0] = fmaf(ssum, u, acc[0]);
-                    acc[1] += svsum;
-                    acc[2] = fmaf(ssum, u * dx, acc[2]);
-                    acc[3] = fmaf(svsum, dx, acc[3]);
-                    acc[4] = fmaf(sv.x, dy.x, fmaf(sv.y, dy.y, acc[4]));
-                    acc[5] += ssum;
+                    Gs = __ffma2_rn(eda[c], mc, Gs);
+                    const float2 ge = __fmul2_rn(g, eda[c]);
+                    const float gsum = ge.x + ge.y;
+                    acc[6 + c * E] += gsum;
+                    if (E == 3) {
+                        acc[6 + c * E + 1] = fmaf(gsum, dx, acc[6 + c * E + 1]);
+                        acc[6 + c * E + 2] = fmaf(ge.x, dy.x, fmaf(ge.y, dy.y, acc[6 + c * E + 2]));
+                    }
+                }
+                const float2 sg = __fmul2_rn(__fmul2_rn(make_float2(-0.5f, -0.5f), g), Gs);
+                const float ssum = sg.x + sg.y;
+                const float2 sv = __fmul2_rn(sg, v);
+                const float svsum = sv.x + sv.y;
+                acc[0] = fmaf(ssum, u, acc[0]);
+                acc[1] += svsum;
+                acc[2] = fmaf(ssum, u * dx, acc[2]);
+                acc[3] = fmaf(svsum, dx, acc[3]);
+                acc[4] = fmaf(sv.x, dy.x, fmaf(sv.y, dy.y, acc[4]));
+                acc[5] += ssum;
             };
             for (int q = lo; q < hi;) {
                 const unsigned e = spw[warp][q];
