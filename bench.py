@@ -275,7 +275,7 @@ def main():
         if fit is None:
             h.step(params, tgt, lr, stats=False)
         else:
-            fit.step(params, tgt, lr)
+            fit.step(params, tgt, lr, stats=False)
 
     flush = None if args.no_flush else L2Flush(dev)
     st0 = h.step(params.clone(), tgt, smoe.LR(0, 0, 0, 0, 0), stats=True)   # calibrate capacity

@@ -37,11 +37,15 @@ constexpr int TILE = 16;                 // 16x16 blocks
 #ifndef SMOE_RASTER_BATCH
 #define SMOE_RASTER_BATCH 128            // kernel records staged per shared-memory batch
 #endif
+#ifndef SMOE_PRE_ATOM
+#define SMOE_PRE_ATOM 4                  // direct binning: count atomics in flight per kernel
+#endif
 #ifndef SMOE_BWD_TWO
 #define SMOE_BWD_TWO 0                   // kernel-parallel backward: two list entries per iteration
 #endif
 constexpr int kFwdUnroll = SMOE_FWD_UNROLL;
 constexpr bool BWD_TWO = SMOE_BWD_TWO != 0;
+constexpr int PRE_ATOM = SMOE_PRE_ATOM;
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int SORT_CAP = 2048;           // bucket size sorted in one smem pass
@@ -232,18 +236,18 @@ preprocess_one(int k, ParamsDev p, float R2, float sx, float sy, int oW, int oH,
         int y0 = max(tb.z, ty_lo), y1 = min(tb.w, ty_hi - 1);
         if (direct) {
             // direct buckets: the count atomic returns k's slot in block t's
-            // fixed-capacity bucket (four atomics in flight per round)
+            // fixed-capacity bucket (PRE_ATOM atomics in flight per round)
             const int wx = tb.y - tb.x + 1, nbx = max(0, y1 - y0 + 1) * wx;
-            for (int i0 = 0; i0 < nbx; i0 += 4) {
-                int t[4], sl[4];
+            for (int i0 = 0; i0 < nbx; i0 += PRE_ATOM) {
+                int t[PRE_ATOM], sl[PRE_ATOM];
 #pragma unroll
-                for (int q = 0; q < 4; q++) {
+                for (int q = 0; q < PRE_ATOM; q++) {
                     const int i = i0 + q, yy = y0 + i / wx, xx = tb.x + i % wx;
                     t[q] = yy * nx + xx;
                     sl[q] = i < nbx ? atomicAdd(&cnt[t[q]], 1) : bcap;
                 }
 #pragma unroll
-                for (int q = 0; q < 4; q++) {
+                for (int q = 0; q < PRE_ATOM; q++) {
                     if (sl[q] < bcap) dids[(size_t)t[q] * bcap + sl[q]] = k;
                     if (i0 + q < nbx) *max_len = max(*max_len, sl[q] + 1);
                 }

@@ -28,11 +28,12 @@ def band_rows(ny: int, rank: int, world: int) -> tuple[int, int]:
     return r0, r1
 
 
-def allreduce_grads(grad: torch.Tensor, sums: torch.Tensor, group=None) -> None:
-    """Sum per-band gradients [K, Pk] (fp32) and loss partials [3] (fp64)
-    over the ranks, in place."""
+def allreduce_grads(grad: torch.Tensor, sums: torch.Tensor | None, group=None) -> None:
+    """Sum per-band gradients [K, Pk] (fp32) and, if given, loss partials [3]
+    (fp64) over the ranks, in place."""
     dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=group)
-    dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
+    if sums is not None:
+        dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
 
 
 class BandedFit:
@@ -51,12 +52,15 @@ class BandedFit:
         self.sums = torch.zeros(3, dtype=torch.float64, device=dev)
         self._smoe = smoe
 
-    def step(self, params, target, lr):
+    def step(self, params, target, lr, stats: bool = True):
+        """One fit iteration; returns the all-reduced loss partials (SSE,
+        clamped SSE, uncovered pixels), or None with stats=False (the loss
+        partials then stay per band: one collective per step, the gradient's)."""
         if self.band[1] > self.band[0]:
             self.h.grad(params, target, self.grad, self.sums)
         else:  # more ranks than block rows: this rank contributes nothing
             self.grad.zero_()
             self.sums.zero_()
-        allreduce_grads(self.grad, self.sums, self.group)
+        allreduce_grads(self.grad, self.sums if stats else None, self.group)
         self.h.apply(params, self.grad, lr)
-        return self.sums
+        return self.sums if stats else None
