@@ -20,6 +20,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <type_traits>
 
 namespace smoe {
 
@@ -981,46 +982,54 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
     };
 
     // ---- forward (Eq. 5 with the per-pixel cull of P:221) ----
-    for (int b0 = 0; b0 < n; b0 += BATCH) {
-        int nb = min(BATCH, n - b0);
-        load_batch(b0, nb);
+    // LIST: also append this warp's list entries (kernel-parallel backward,
+    // K_n within one batch); a separate instantiation keeps the test out of
+    // the kernel loop
+    auto forward = [&](auto list_tag) {
+        constexpr bool LIST = decltype(list_tag)::value;
+        for (int b0 = 0; b0 < n; b0 += BATCH) {
+            int nb = min(BATCH, n - b0);
+            load_batch(b0, nb);
 #pragma unroll FWD_UNROLL
-        for (int j = 0; j < nb; j++) {
-            float r[R::RS];
-            load_rec(j, r);
-            float dx, u;
-            float2 dy, w, q;
-            dist2(r, dx, dy, u, w, q);
-            bool h0 = v0 && q.x <= R2, h1 = v1 && q.y <= R2;
-            unsigned b0m = __ballot_sync(FULL, h0), b1m = __ballot_sync(FULL, h1);
-            if (PROF) {
-                w_tested += w_valid;
-                w_hit += __popc(b0m) + __popc(b1m);
-            }
-            if ((b0m | b1m) == 0u) continue;
-            if (MASKS && n <= BATCH) {
-                // this warp's lanes with a pixel inside kernel j's ellipse,
-                // appended to its list (one entry per lane = pixel pair)
-                const unsigned bm = b0m | b1m;
-                const int p0 = wrun + __popc(bm & lt);
-                if ((h0 || h1) && p0 < CAPW)
-                    spw[warp][p0] = (unsigned short)(((unsigned)j << 7) | ebits | (h1 ? 2u : 0u) | (h0 ? 1u : 0u));
-                wrun += __popc(bm);
-            }
-            const float2 ea = __ffma2_rn(q, make_float2(-0.5f * LOG2E, -0.5f * LOG2E), make_float2(r[5], r[5]));
-            const float2 g = make_float2(h0 ? ex2_approx(ea.x) : 0.f, h1 ? ex2_approx(ea.y) : 0.f);
-            D2 = __fadd2_rn(D2, g);
-#pragma unroll
-            for (int c = 0; c < C; c++) {
-                float2 m = make_float2(r[6 + c * E], r[6 + c * E]);
-                if (E == 3) {
-                    const float mb = fmaf(r[6 + c * E + 1], dx, r[6 + c * E]);
-                    m = __ffma2_rn(make_float2(r[6 + c * E + 2], r[6 + c * E + 2]), dy, make_float2(mb, mb));
+            for (int j = 0; j < nb; j++) {
+                float r[R::RS];
+                load_rec(j, r);
+                float dx, u;
+                float2 dy, w, q;
+                dist2(r, dx, dy, u, w, q);
+                bool h0 = v0 && q.x <= R2, h1 = v1 && q.y <= R2;
+                unsigned b0m = __ballot_sync(FULL, h0), b1m = __ballot_sync(FULL, h1);
+                if (PROF) {
+                    w_tested += w_valid;
+                    w_hit += __popc(b0m) + __popc(b1m);
                 }
-                N2[c] = __ffma2_rn(g, m, N2[c]);
+                if ((b0m | b1m) == 0u) continue;
+                if (LIST) {
+                    // this warp's lanes with a pixel inside kernel j's ellipse,
+                    // appended to its list (one entry per lane = pixel pair)
+                    const unsigned bm = b0m | b1m;
+                    const unsigned hm = (h0 ? 1u : 0u) | (h1 ? 2u : 0u);
+                    const int p0 = wrun + __popc(bm & lt);
+                    if (hm != 0u && p0 < CAPW) spw[warp][p0] = (unsigned short)(((unsigned)j << 7) | ebits | hm);
+                    wrun += __popc(bm);
+                }
+                const float2 ea = __ffma2_rn(q, make_float2(-0.5f * LOG2E, -0.5f * LOG2E), make_float2(r[5], r[5]));
+                const float2 g = make_float2(h0 ? ex2_approx(ea.x) : 0.f, h1 ? ex2_approx(ea.y) : 0.f);
+                D2 = __fadd2_rn(D2, g);
+#pragma unroll
+                for (int c = 0; c < C; c++) {
+                    float2 m = make_float2(r[6 + c * E], r[6 + c * E]);
+                    if (E == 3) {
+                        const float mb = fmaf(r[6 + c * E + 1], dx, r[6 + c * E]);
+                        m = __ffma2_rn(make_float2(r[6 + c * E + 2], r[6 + c * E + 2]), dy, make_float2(mb, mb));
+                    }
+                    N2[c] = __ffma2_rn(g, m, N2[c]);
+                }
             }
         }
-    }
+    };
+    if (MASKS && n <= BATCH) forward(std::true_type{});
+    else forward(std::false_type{});
     if (PROF && lane == 0) {
         atomicAdd(&A.work[0], w_tested);
         atomicAdd(&A.work[1], w_hit);
