@@ -1203,6 +1203,7 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
             int cj = -1;
             float4 *dst = nullptr;
             float r[R::RS];
+            float bx = 0.f, by = 0.f;   // quadrant origin - kernel centre
             float acc[R::P];
 #pragma unroll
             for (int i = 0; i < R::P; i++) acc[i] = 0.f;
@@ -1210,8 +1211,8 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
             auto add_entry = [&](const unsigned e) {
                 const int l = (int)((e >> 2) & 31u);
                 const float4 pa = spw_pix[2 * l], pb = spw_pix[2 * l + 1];
-                const float dx = xw + (float)(l & 7) - r[0];
-                const float yl = yw + (float)((l >> 3) * 2) - r[1];
+                const float dx = bx + (float)(l & 7);
+                const float yl = by + (float)((l >> 3) * 2);
                 const float2 dy = make_float2(yl, yl + 1.0f);
                 const float u = r[2] * dx;
                 const float bdx = r[3] * dx;
@@ -1268,6 +1269,8 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
                     cj = j;
                     dst = reinterpret_cast<float4 *>(A.acc + (size_t)sid[j] * R::V);
                     load_rec(j, r);
+                    bx = xw - r[0];
+                    by = yw - r[1];
                 }
                 if (BWD_TWO) {
                     // a second entry of the same kernel in the same iteration
