@@ -223,6 +223,44 @@ class L2Flush:
         torch.sum(self.r, dim=0, out=self.s)
 
 
+def e2e_banded(fit, params, target, T_total, steps, dev):
+    """e2e at N>1 through the public API (BandedFit.step with a pinned HOST
+    target): each rank's smoe_grad copies only its band's pixel rows to the
+    device (double-buffered copy stream), the gradient and loss partials are
+    all-reduced, and every step's loss partials come back to pinned host
+    memory (read two steps later).  Wall time per rank, max over ranks."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2510_05814_b200 import smoe
+    host_t = torch.as_tensor(target).pin_memory()
+    n = min(steps, 500)
+    ring = torch.empty((4, 3), dtype=torch.float64).pin_memory()
+    evs = [torch.cuda.Event() for _ in range(4)]
+    lag, losses = 2, []
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for i in range(n):
+        sums = fit.step(params, host_t, smoe.LR.paper(T_total, T_total), stats=True)
+        ring[i % 4].copy_(sums, non_blocking=True)
+        evs[i % 4].record()
+        if i >= lag:
+            evs[(i - lag) % 4].synchronize()
+            losses.append(float(ring[(i - lag) % 4][0]))
+    torch.cuda.synchronize()
+    for i in range(max(0, n - lag), n):
+        losses.append(float(ring[i % 4][0]))
+    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    assert len(losses) == n and all(np.isfinite(losses))
+    r0, r1 = fit.band
+    return {"value": n / float(dt.item()), "unit": "it/s", "h2d_bytes_per_step": int(target.nbytes),
+            "d2h_bytes_per_step": 24 * fit.world, "steps": n,
+            "note": "each rank: pinned H2D of its band's target rows (double-buffered copy stream), gradient + "
+                    "loss all-reduce, async D2H of the reduced loss partials; bytes summed over ranks, time max over ranks"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -234,6 +272,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="N>1 process group; gloo (CUDA tensors) lets several ranks share one GPU in tests")
     ap.add_argument("--K", type=int, default=0, help="override the config's kernel count (density sweeps; not a bench line)")
     ap.add_argument("--backward-mode", type=int, default=-1, help="-1 auto (default), 0 pixel-parallel, 1 kernel-parallel")
     ap.add_argument("--no-profile", action="store_true", help="no per-kernel events in the timed region")
@@ -255,9 +295,13 @@ def main():
     from paper_2510_05814_b200.dist import BandedFit
 
     rank, world, local = rank_env()
+    local = local % torch.cuda.device_count()       # ranks may share a GPU under --dist-backend gloo
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     cfg = dict(synth.CONFIGS[args.config])
     if args.K > 0:
         cfg["K"] = args.K
@@ -405,6 +449,8 @@ def main():
     # H2D of step t+1 overlaps the compute of step t) and reads its loss/PSNR
     # back (smoe_stats_async into a pinned ring, consumed two steps later)
     e2e = None
+    if not args.no_e2e and world > 1:
+        e2e = e2e_banded(fit, params, target, T_total, args.steps, dev)
     if not args.no_e2e and world == 1:
         host_t = torch.as_tensor(target).pin_memory()
         n_e2e = min(args.steps, 500)

@@ -168,7 +168,9 @@ smoe_status smoe_set_band(smoe_handle h, int tile_row0, int tile_row1);
 /* Gradient of the loss restricted to the current band: grad[K][Pk] float32
  * with Pk = 6 + C E, per kernel (mu_x, mu_y, l11, l21, l22, log_pi, expert
  * block in the expert layout); sums[3] float64 = (SSE, clamped SSE, uncovered
- * pixels) of the band.  grad and sums may be host or device pointers. */
+ * pixels) of the band.  grad and sums may be host or device pointers.
+ * target[C][H][W] is the full image; a host target has only the band's
+ * pixel rows copied to the device (the other rows are never read). */
 smoe_status smoe_grad(smoe_handle h, const smoe_params *p, const float *target,
                       float *grad, double *sums);
 

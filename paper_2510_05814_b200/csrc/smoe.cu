@@ -517,7 +517,19 @@ const float *stage_target(smoe_ctx *h, const float *target)
     const int s = h->tslot;
     h->tslot ^= 1;
     CK(cudaStreamWaitEvent(h->copy_stream, h->tconsumed[s], 0));      // buffer no longer read
-    CK(cudaMemcpyAsync(h->tstage[s], target, n * sizeof(float), cudaMemcpyHostToDevice, h->copy_stream));
+    int ty_lo, ty_hi;
+    band_rows(h, ty_lo, ty_hi);
+    const int r0 = ty_lo * TILE, r1 = std::min(ty_hi * TILE, h->H);
+    if (r0 == 0 && r1 == h->H) {
+        CK(cudaMemcpyAsync(h->tstage[s], target, n * sizeof(float), cudaMemcpyHostToDevice, h->copy_stream));
+    } else {
+        // a band reads only its own pixel rows: copy those, one row of the
+        // 2D copy per channel (pitch H*W floats)
+        const size_t off = (size_t)r0 * h->W, pitch = (size_t)h->H * h->W * sizeof(float);
+        CK(cudaMemcpy2DAsync(h->tstage[s] + off, pitch, target + off, pitch,
+                             (size_t)(r1 - r0) * h->W * sizeof(float), h->C, cudaMemcpyHostToDevice,
+                             h->copy_stream));
+    }
     CK(cudaEventRecord(h->tcopied[s], h->copy_stream));
     CK(cudaStreamWaitEvent(h->stream, h->tcopied[s], 0));
     h->tpending = s;

@@ -87,3 +87,26 @@ def test_two_ranks_one_gpu_match_single_process():
     close = np.abs(res[0][2] - ref) <= 1e-2 * lrv[None, :] * STEPS + 1e-6 * np.abs(ref)
     assert close.mean() > 0.99
     assert np.all(np.abs(res[0][2] - ref) <= 2.0 * lrv[None, :] * STEPS + 1e-6 * np.abs(ref))
+
+
+def test_band_host_target_copies_band_rows_only():
+    """A banded smoe_grad with a HOST target stages only the band's rows; the
+    result equals the device-target call (up to the order of the gradient
+    atomics) for every band, including the clipped last one."""
+    from paper_2510_05814_b200 import smoe
+    target, pool = _inputs()
+    p = smoe.Params.from_numpy(pool, "cuda:0")
+    tg = torch.as_tensor(target).cuda()
+    host = torch.as_tensor(target).pin_memory()
+    for band in [(0, 2), (2, 5), (5, 6)]:
+        h = smoe.SMoE(K, H, W, C, 1)
+        h.set_band(*band)
+        gd, sd = h.grad(p, tg)
+        gh, sh = h.grad(p, host)
+        gh2, sh2 = h.grad(p, host)          # second staging buffer
+        torch.cuda.synchronize()
+        tol = 1e-5 * float(gd.abs().max())
+        for g, s in [(gh, sh), (gh2, sh2)]:
+            assert torch.allclose(g, gd, rtol=1e-4, atol=tol)
+            assert torch.allclose(s, sd, rtol=1e-6, atol=0)
+        assert float(sd[0]) > 0
