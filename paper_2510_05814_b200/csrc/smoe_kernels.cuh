@@ -41,11 +41,29 @@ constexpr int TILE = 16;                 // 16x16 blocks
 #ifndef SMOE_PRE_ATOM
 #define SMOE_PRE_ATOM 4                  // direct binning: count atomics in flight per kernel
 #endif
+#ifndef SMOE_ASM_LDS
+#define SMOE_ASM_LDS 1                   // backward: pixel seeds loaded through a 32-bit shared address
+#endif
 #ifndef SMOE_BWD_TWO
 #define SMOE_BWD_TWO 0                   // kernel-parallel backward: two list entries per iteration
 #endif
 constexpr int kFwdUnroll = SMOE_FWD_UNROLL;
 constexpr bool BWD_TWO = SMOE_BWD_TWO != 0;
+
+// 128-bit shared load from a 32-bit shared-window address (keeps the
+// generic-to-shared conversion out of the backward loop)
+__device__ __forceinline__ float4 lds128(unsigned a)
+{
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int lds32(unsigned a)
+{
+    int v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
 constexpr int PRE_ATOM = SMOE_PRE_ATOM;
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr unsigned FULL = 0xffffffffu;
@@ -913,7 +931,9 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
     // [warp][lane] = {(eD_0, eD_0'), (eD_1, eD_1')}, {(eD_2, eD_2'), (K, K')}
     __shared__ float4 spix[MASKS ? 256 : 1];
     constexpr int CAPW = 2048;                    // per-warp pair-list capacity (window)
-    // list entry: (kernel << 7) | (lane << 2) | (lower pixel hit << 1) | upper pixel hit
+    // list entry: (kernel << 7) | (lower pixel hit << 6) | (upper pixel hit << 5) | lane
+    // (lane in the low bits: the seed address and the pixel offsets decode
+    // with one mask each)
     __shared__ unsigned short spw[MASKS ? 4 : 1][MASKS ? CAPW : 1];
     __shared__ double red[3][4];
 
@@ -947,7 +967,7 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
     unsigned long long w_tested = 0, w_hit = 0;
     int wrun = 0;                                  // pairs this warp listed (KPAR)
     const unsigned lt = (1u << lane) - 1u;
-    const unsigned ebits = (unsigned)lane << 2;
+    const unsigned ebits = (unsigned)lane;
     const int w_valid = PROF ? __popc(__ballot_sync(FULL, v0)) + __popc(__ballot_sync(FULL, v1)) : 0;
 
     auto load_batch = [&](int b0, int nb) {
@@ -1008,7 +1028,7 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
                     // this warp's lanes with a pixel inside kernel j's ellipse,
                     // appended to its list (one entry per lane = pixel pair)
                     const unsigned bm = b0m | b1m;
-                    const unsigned hm = (h0 ? 1u : 0u) | (h1 ? 2u : 0u);
+                    const unsigned hm = (h0 ? 0x20u : 0u) | (h1 ? 0x40u : 0u);
                     const int p0 = wrun + __popc(bm & lt);
                     if (hm != 0u && p0 < CAPW) spw[warp][p0] = (unsigned short)(((unsigned)j << 7) | ebits | hm);
                     wrun += __popc(bm);
@@ -1172,6 +1192,8 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
     // and at the end of its range.
     const float xw = (float)(tx * TILE + (warp & 1) * 8), yw = (float)(ty * TILE + (warp >> 1) * 8);
     const float4 *spw_pix = spix + warp * 64;   // this warp's lanes' seeds
+    const unsigned spw_pix_s = (unsigned)__cvta_generic_to_shared(spw_pix);
+    const unsigned srec_s = (unsigned)__cvta_generic_to_shared(srec), sid_s = (unsigned)__cvta_generic_to_shared(sid);
     for (int b0 = 0; b0 < n; b0 += BATCH) {
         int nb = min(BATCH, n - b0);
         int total = wrun;                      // n <= BATCH: listed by the forward
@@ -1191,7 +1213,7 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
                     const unsigned bm = __ballot_sync(FULL, h0 || h1);
                     const int p0 = run + __popc(bm & lt) - q0;
                     if ((h0 || h1) && p0 >= 0 && p0 < CAPW)
-                        spw[warp][p0] = (unsigned short)(((unsigned)j << 7) | ebits | (h1 ? 2u : 0u) | (h0 ? 1u : 0u));
+                        spw[warp][p0] = (unsigned short)(((unsigned)j << 7) | ebits | (h1 ? 0x40u : 0u) | (h0 ? 0x20u : 0u));
                     run += __popc(bm);
                 }
                 total = run;
@@ -1209,8 +1231,16 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
             for (int i = 0; i < R::P; i++) acc[i] = 0.f;
             // one entry's contribution to the raw sums (a pixel outside the ellipse: g = 0)
             auto add_entry = [&](const unsigned e) {
-                const int l = (int)((e >> 2) & 31u);
-                const float4 pa = spw_pix[2 * l], pb = spw_pix[2 * l + 1];
+                const int l = (int)(e & 31u);
+                float4 pa, pb;
+                if (SMOE_ASM_LDS) {
+                    const unsigned a = spw_pix_s + ((e & 31u) << 5);   // + 32 l bytes
+                    pa = lds128(a);
+                    pb = lds128(a + 16u);
+                } else {
+                    pa = spw_pix[2 * l];
+                    pb = spw_pix[2 * l + 1];
+                }
                 const float dx = bx + (float)(l & 7);
                 const float yl = by + (float)((l >> 3) * 2);
                 const float2 dy = make_float2(yl, yl + 1.0f);
@@ -1220,7 +1250,7 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
                 const float uu = u * u;
                 const float2 qd = __ffma2_rn(v, v, make_float2(uu, uu));
                 const float2 ea = __ffma2_rn(qd, make_float2(-0.5f * LOG2E, -0.5f * LOG2E), make_float2(r[5], r[5]));
-                const float2 g = make_float2((e & 1u) ? ex2_approx(ea.x) : 0.f, (e & 2u) ? ex2_approx(ea.y) : 0.f);
+                const float2 g = make_float2((e & 0x20u) ? ex2_approx(ea.x) : 0.f, (e & 0x40u) ? ex2_approx(ea.y) : 0.f);
                 const float2 eda[4] = {make_float2(pa.x, pa.y), make_float2(pa.z, pa.w),
                                        make_float2(pb.x, pb.y), make_float2(pb.z, pb.w)};
                 float2 Gs = make_float2(-eda[3].x, -eda[3].y);
@@ -1267,8 +1297,17 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
                         for (int i = 0; i < R::P; i++) acc[i] = 0.f;
                     }
                     cj = j;
-                    dst = reinterpret_cast<float4 *>(A.acc + (size_t)sid[j] * R::V);
-                    load_rec(j, r);
+                    if (SMOE_ASM_LDS) {
+                        dst = reinterpret_cast<float4 *>(A.acc + (size_t)lds32(sid_s + 4u * j) * R::V);
+#pragma unroll
+                        for (int q4 = 0; q4 < RS4; q4++) {
+                            const float4 f = lds128(srec_s + 16u * (j * RS4 + q4));
+                            r[4 * q4] = f.x; r[4 * q4 + 1] = f.y; r[4 * q4 + 2] = f.z; r[4 * q4 + 3] = f.w;
+                        }
+                    } else {
+                        dst = reinterpret_cast<float4 *>(A.acc + (size_t)sid[j] * R::V);
+                        load_rec(j, r);
+                    }
                     bx = xw - r[0];
                     by = yw - r[1];
                 }
@@ -1277,7 +1316,7 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
                     // (or a null one: same lane, no pixel)
                     unsigned e2 = (q + 1 < hi) ? spw[warp][q + 1] : 0u;
                     const bool two = q + 1 < hi && (int)(e2 >> 7) == j;
-                    if (!two) e2 = e & ~3u;
+                    if (!two) e2 = e & ~0x60u;
                     q += two ? 2 : 1;
                     add_entry(e);
                     add_entry(e2);
