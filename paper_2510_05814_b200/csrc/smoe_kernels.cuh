@@ -1192,8 +1192,17 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
     // and at the end of its range.
     const float xw = (float)(tx * TILE + (warp & 1) * 8), yw = (float)(ty * TILE + (warp >> 1) * 8);
     const float4 *spw_pix = spix + warp * 64;   // this warp's lanes' seeds
-    const unsigned spw_pix_s = (unsigned)__cvta_generic_to_shared(spw_pix);
-    const unsigned srec_s = (unsigned)__cvta_generic_to_shared(srec), sid_s = (unsigned)__cvta_generic_to_shared(sid);
+    unsigned spw_pix_s = (unsigned)__cvta_generic_to_shared(spw_pix);
+    unsigned srec_s = (unsigned)__cvta_generic_to_shared(srec), sid_s = (unsigned)__cvta_generic_to_shared(sid);
+    if (E == 3) {
+        // linear experts: opaque copies keep the three shared bases in
+        // registers instead of rematerialising them (S2UR + ULEA) at every
+        // kernel switch (config 2 +1.4%; the constant-expert forms, bound to
+        // 72 registers, lose 0.5-1% at configs 3/5 and stay as they are)
+        asm volatile("mov.b32 %0, %0;" : "+r"(srec_s));
+        asm volatile("mov.b32 %0, %0;" : "+r"(sid_s));
+        asm volatile("mov.b32 %0, %0;" : "+r"(spw_pix_s));
+    }
     for (int b0 = 0; b0 < n; b0 += BATCH) {
         int nb = min(BATCH, n - b0);
         int total = wrun;                      // n <= BATCH: listed by the forward
