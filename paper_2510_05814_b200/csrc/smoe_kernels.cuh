@@ -44,11 +44,7 @@ constexpr int TILE = 16;                 // 16x16 blocks
 #ifndef SMOE_ASM_LDS
 #define SMOE_ASM_LDS 1                   // backward: pixel seeds loaded through a 32-bit shared address
 #endif
-#ifndef SMOE_BWD_TWO
-#define SMOE_BWD_TWO 0                   // kernel-parallel backward: two list entries per iteration
-#endif
 constexpr int kFwdUnroll = SMOE_FWD_UNROLL;
-constexpr bool BWD_TWO = SMOE_BWD_TWO != 0;
 
 // 128-bit shared load from a 32-bit shared-window address (keeps the
 // generic-to-shared conversion out of the backward loop)
@@ -930,11 +926,10 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
     // per-lane backward seeds of the lane's pixel pair, packed by pixel:
     // [warp][lane] = {(eD_0, eD_0'), (eD_1, eD_1')}, {(eD_2, eD_2'), (K, K')}
     __shared__ float4 spix[MASKS ? 256 : 1];
-    constexpr int CAPW = 2048;                    // per-warp pair-list capacity (window)
-    // list entry: (kernel << 7) | (lower pixel hit << 6) | (upper pixel hit << 5) | lane
-    // (lane in the low bits: the seed address and the pixel offsets decode
-    // with one mask each)
-    __shared__ unsigned short spw[MASKS ? 4 : 1][MASKS ? CAPW : 1];
+    // per-warp kernel records of the pair list: {upper-pixel ballot, lower-pixel
+    // ballot, kernel slot in the batch, entries before it}; a lane with either
+    // pixel inside is one entry (a vertical pixel pair)
+    __shared__ uint4 skr[MASKS ? 4 : 1][MASKS ? BATCH : 1];
     __shared__ double red[3][4];
 
     const int tx = tile % A.nx, ty = tile / A.nx;
@@ -965,9 +960,7 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
 #pragma unroll
     for (int c = 0; c < C; c++) N2[c] = make_float2(0.f, 0.f);
     unsigned long long w_tested = 0, w_hit = 0;
-    int wrun = 0;                                  // pairs this warp listed (KPAR)
-    const unsigned lt = (1u << lane) - 1u;
-    const unsigned ebits = (unsigned)lane;
+    int wrun = 0, nrec = 0;                        // entries / kernel records this warp listed (KPAR)
     const int w_valid = PROF ? __popc(__ballot_sync(FULL, v0)) + __popc(__ballot_sync(FULL, v1)) : 0;
 
     auto load_batch = [&](int b0, int nb) {
@@ -1025,13 +1018,11 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
                 }
                 if ((b0m | b1m) == 0u) continue;
                 if (LIST) {
-                    // this warp's lanes with a pixel inside kernel j's ellipse,
-                    // appended to its list (one entry per lane = pixel pair)
-                    const unsigned bm = b0m | b1m;
-                    const unsigned hm = (h0 ? 0x20u : 0u) | (h1 ? 0x40u : 0u);
-                    const int p0 = wrun + __popc(bm & lt);
-                    if (hm != 0u && p0 < CAPW) spw[warp][p0] = (unsigned short)(((unsigned)j << 7) | ebits | hm);
-                    wrun += __popc(bm);
+                    // one record per (warp, kernel) with a hit: its two
+                    // ballots and the entries listed before it
+                    if (lane == 0) skr[warp][nrec] = make_uint4(b0m, b1m, (unsigned)j, (unsigned)wrun);
+                    nrec++;
+                    wrun += __popc(b0m | b1m);
                 }
                 const float2 ea = __ffma2_rn(q, make_float2(-0.5f * LOG2E, -0.5f * LOG2E), make_float2(r[5], r[5]));
                 const float2 g = make_float2(h0 ? ex2_approx(ea.x) : 0.f, h1 ? ex2_approx(ea.y) : 0.f);
@@ -1205,45 +1196,94 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
     }
     for (int b0 = 0; b0 < n; b0 += BATCH) {
         int nb = min(BATCH, n - b0);
-        int total = wrun;                      // n <= BATCH: listed by the forward
-        if (n > BATCH) load_batch(b0, nb);
-        for (int q0 = 0; q0 < total || (n > BATCH && q0 == 0); q0 += CAPW) {
-            if (n > BATCH || q0 > 0) {
-                // (re)build the warp's list window [q0, q0 + CAPW) for the
-                // resident batch: the cull test again, entries in window kept
-                int run = 0;
-                for (int j = 0; j < nb; j++) {
-                    float rb[R::RS];
-                    load_rec(j, rb);
-                    float dx, u;
-                    float2 dyv, wv, qv;
-                    dist2(rb, dx, dyv, u, wv, qv);
-                    bool h0 = v0 && qv.x <= R2, h1 = v1 && qv.y <= R2;
-                    const unsigned bm = __ballot_sync(FULL, h0 || h1);
-                    const int p0 = run + __popc(bm & lt) - q0;
-                    if ((h0 || h1) && p0 >= 0 && p0 < CAPW)
-                        spw[warp][p0] = (unsigned short)(((unsigned)j << 7) | ebits | (h1 ? 0x40u : 0u) | (h0 ? 0x20u : 0u));
-                    run += __popc(bm);
-                }
-                total = run;
-                __syncwarp();
+        int total = wrun, nr = nrec;           // n <= BATCH: listed by the forward
+        if (n > BATCH) {
+            load_batch(b0, nb);
+            // rebuild the warp's kernel records for the resident batch
+            total = 0;
+            nr = 0;
+            for (int j = 0; j < nb; j++) {
+                float rb[R::RS];
+                load_rec(j, rb);
+                float dx, u;
+                float2 dyv, wv, qv;
+                dist2(rb, dx, dyv, u, wv, qv);
+                const unsigned c0 = __ballot_sync(FULL, v0 && qv.x <= R2), c1 = __ballot_sync(FULL, v1 && qv.y <= R2);
+                if ((c0 | c1) == 0u) continue;
+                if (lane == 0) skr[warp][nr] = make_uint4(c0, c1, (unsigned)j, (unsigned)total);
+                nr++;
+                total += __popc(c0 | c1);
             }
-            if (q0 >= total) break;
-            const int Tw = min(total - q0, CAPW);
-            const int lo = (lane * Tw) >> 5, hi = ((lane + 1) * Tw) >> 5;
-            int cj = -1;
-            float4 *dst = nullptr;
+        }
+        __syncwarp();
+        // lane range [lo, hi) of the warp's entries (kernel-major)
+        const int lo = (lane * total) >> 5, hi = ((lane + 1) * total) >> 5;
+        if (lo < hi) {
+            // the record holding entry lo: last record with prefix <= lo
+            int ra = 0;
+            for (int step = 64; step >= 1; step >>= 1)
+                if (ra + step < nr && (int)skr[warp][ra + step].w <= lo) ra += step;
+            uint4 kr = skr[warp][ra];
+            unsigned m = kr.x | kr.y;
+            {
+                // drop the record's first (lo - prefix) entries: position of
+                // its (k+1)-th set bit by a binary search on popcounts
+                const int k = lo - (int)kr.w;
+                int t = 0;
+#pragma unroll
+                for (int sft = 16; sft >= 1; sft >>= 1)
+                    if (__popc(m & ((1u << (t + sft)) - 1u)) <= k) t += sft;
+                m &= ~((1u << t) - 1u);
+            }
+            float4 *dst;
             float r[R::RS];
-            float bx = 0.f, by = 0.f;   // quadrant origin - kernel centre
+            float bx, by;                       // quadrant origin - kernel centre
             float acc[R::P];
 #pragma unroll
             for (int i = 0; i < R::P; i++) acc[i] = 0.f;
-            // one entry's contribution to the raw sums (a pixel outside the ellipse: g = 0)
-            auto add_entry = [&](const unsigned e) {
-                const int l = (int)(e & 31u);
+            auto open_kernel = [&](int j) {
+                if (SMOE_ASM_LDS) {
+                    dst = reinterpret_cast<float4 *>(A.acc + (size_t)lds32(sid_s + 4u * j) * R::V);
+#pragma unroll
+                    for (int q4 = 0; q4 < RS4; q4++) {
+                        const float4 f = lds128(srec_s + 16u * (j * RS4 + q4));
+                        r[4 * q4] = f.x; r[4 * q4 + 1] = f.y; r[4 * q4 + 2] = f.z; r[4 * q4 + 3] = f.w;
+                    }
+                } else {
+                    dst = reinterpret_cast<float4 *>(A.acc + (size_t)sid[j] * R::V);
+                    load_rec(j, r);
+                }
+                bx = xw - r[0];
+                by = yw - r[1];
+            };
+            auto flush = [&] {
+#pragma unroll
+                for (int q4 = 0; q4 < (R::P + 3) / 4; q4++) {
+                    float t4[4];
+#pragma unroll
+                    for (int k4 = 0; k4 < 4; k4++) t4[k4] = (4 * q4 + k4 < R::P) ? acc[4 * q4 + k4] : 0.f;
+                    atomicAdd(dst + q4, make_float4(t4[0], t4[1], t4[2], t4[3]));
+                }
+            };
+            open_kernel((int)kr.z);
+            for (int q = lo; q < hi; q++) {
+                if (m == 0u) {
+                    // kernel switch: flush this kernel's sums, open the next record
+                    flush();
+#pragma unroll
+                    for (int i = 0; i < R::P; i++) acc[i] = 0.f;
+                    kr = skr[warp][++ra];
+                    m = kr.x | kr.y;
+                    open_kernel((int)kr.z);
+                }
+                const unsigned lb = m & (0u - m);       // lowest listed lane
+                m ^= lb;
+                const int l = 31 - __clz(lb);
+                const bool g0 = (kr.x & lb) != 0u, g1 = (kr.y & lb) != 0u;
+                // this pair's contribution to the raw sums (a pixel outside the ellipse: g = 0)
                 float4 pa, pb;
                 if (SMOE_ASM_LDS) {
-                    const unsigned a = spw_pix_s + ((e & 31u) << 5);   // + 32 l bytes
+                    const unsigned a = spw_pix_s + ((unsigned)l << 5);   // + 32 l bytes
                     pa = lds128(a);
                     pb = lds128(a + 16u);
                 } else {
@@ -1259,7 +1299,7 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
                 const float uu = u * u;
                 const float2 qd = __ffma2_rn(v, v, make_float2(uu, uu));
                 const float2 ea = __ffma2_rn(qd, make_float2(-0.5f * LOG2E, -0.5f * LOG2E), make_float2(r[5], r[5]));
-                const float2 g = make_float2((e & 0x20u) ? ex2_approx(ea.x) : 0.f, (e & 0x40u) ? ex2_approx(ea.y) : 0.f);
+                const float2 g = make_float2(g0 ? ex2_approx(ea.x) : 0.f, g1 ? ex2_approx(ea.y) : 0.f);
                 const float2 eda[4] = {make_float2(pa.x, pa.y), make_float2(pa.z, pa.w),
                                        make_float2(pb.x, pb.y), make_float2(pb.z, pb.w)};
                 float2 Gs = make_float2(-eda[3].x, -eda[3].y);
@@ -1289,61 +1329,8 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
                 acc[3] = fmaf(svsum, dx, acc[3]);
                 acc[4] = fmaf(sv.x, dy.x, fmaf(sv.y, dy.y, acc[4]));
                 acc[5] += ssum;
-            };
-            for (int q = lo; q < hi;) {
-                const unsigned e = spw[warp][q];
-                const int j = (int)(e >> 7);
-                if (j != cj) {
-                    if (cj >= 0) {
-#pragma unroll
-                        for (int q4 = 0; q4 < (R::P + 3) / 4; q4++) {
-                            float t4[4];
-#pragma unroll
-                            for (int k4 = 0; k4 < 4; k4++) t4[k4] = (4 * q4 + k4 < R::P) ? acc[4 * q4 + k4] : 0.f;
-                            atomicAdd(dst + q4, make_float4(t4[0], t4[1], t4[2], t4[3]));
-                        }
-#pragma unroll
-                        for (int i = 0; i < R::P; i++) acc[i] = 0.f;
-                    }
-                    cj = j;
-                    if (SMOE_ASM_LDS) {
-                        dst = reinterpret_cast<float4 *>(A.acc + (size_t)lds32(sid_s + 4u * j) * R::V);
-#pragma unroll
-                        for (int q4 = 0; q4 < RS4; q4++) {
-                            const float4 f = lds128(srec_s + 16u * (j * RS4 + q4));
-                            r[4 * q4] = f.x; r[4 * q4 + 1] = f.y; r[4 * q4 + 2] = f.z; r[4 * q4 + 3] = f.w;
-                        }
-                    } else {
-                        dst = reinterpret_cast<float4 *>(A.acc + (size_t)sid[j] * R::V);
-                        load_rec(j, r);
-                    }
-                    bx = xw - r[0];
-                    by = yw - r[1];
-                }
-                if (BWD_TWO) {
-                    // a second entry of the same kernel in the same iteration
-                    // (or a null one: same lane, no pixel)
-                    unsigned e2 = (q + 1 < hi) ? spw[warp][q + 1] : 0u;
-                    const bool two = q + 1 < hi && (int)(e2 >> 7) == j;
-                    if (!two) e2 = e & ~0x60u;
-                    q += two ? 2 : 1;
-                    add_entry(e);
-                    add_entry(e2);
-                } else {
-                    q++;
-                    add_entry(e);
-                }
             }
-            if (cj >= 0) {
-#pragma unroll
-                for (int q4 = 0; q4 < (R::P + 3) / 4; q4++) {
-                    float t4[4];
-#pragma unroll
-                    for (int k4 = 0; k4 < 4; k4++) t4[k4] = (4 * q4 + k4 < R::P) ? acc[4 * q4 + k4] : 0.f;
-                    atomicAdd(dst + q4, make_float4(t4[0], t4[1], t4[2], t4[3]));
-                }
-            }
-            __syncwarp();
+            flush();
         }
         __syncthreads();
     }
