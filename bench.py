@@ -4,11 +4,14 @@
 Metric (BASELINE.json): "SMoE fit iterations/s and render Mpix/s at 1/2/4/8
 B200 (% of roofline)".  One bench step = one fit iteration of the whole hot
 path (§8(a) a1-a8: preprocess, binning, forward, loss, backward, Adam) over
-the configured synthetic workload; the render (a9) is timed separately and
-reported under "render".  Default workload: BASELINE.json config 2 (768x512
-RGB Kodak-shaped synthetic image, 10k kernels, linear experts; the metric's
-configuration).  N > 1 (torchrun): tile-row bands per rank, NCCL all-reduce
-of the gradients every step (paper_2510_05814_b200/dist.py).
+the configured synthetic workload; the render (a9) is timed separately, on
+the fitted model, and reported under "render".  Default workload:
+BASELINE.json config 3 (2040x1356 RGB DIV2K-shaped synthetic image, 100k
+kernels, 2000-iteration fit + 4x native super-resolution render), the
+largest configuration that fits one GPU (config 5 is the multi-GPU one).
+N > 1 (torchrun): tile-row bands per rank, reduce-scatter of the gradients,
+sharded Adam, all-gather of the parameters every step
+(paper_2510_05814_b200/dist.py).
 
 Timing: W warm-up steps; then K steps, each bracketed by CUDA events on the
 launch stream with an L2 flush (256 MB write + 256 MB read) between steps outside the
@@ -92,21 +95,41 @@ def rank_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
+def cpu_info():
+    """Host CPU model and core count (the cpu_baseline's context)."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
 def cpu_oracle_sample(target, pool, rows):
     """Time the CPU oracle's loss+gradient on image rows [r0, r1) (dense over
-    all kernels, fp64, one thread) plus its Adam step.  Returns (seconds for
-    the rows, seconds for Adam)."""
+    all kernels, fp64, one thread) plus its Adam step, pinned to one core
+    (the equivalent of taskset -c <core>).  Returns (seconds for the rows,
+    seconds for Adam, the core)."""
     import numpy as np
     import oracle as O
     op = O.Params.from_any(pool)
     t = target.astype(np.float64)
-    t0 = time.perf_counter()
-    lg = O.loss_grad(op, t, rows=rows)
-    t1 = time.perf_counter()
-    opt = O.Adam(op.K, op.Pk)
-    opt.step(op, lg.grad, O.LR())
-    t2 = time.perf_counter()
-    return t1 - t0, t2 - t1
+    old = os.sched_getaffinity(0)
+    core = min(old)
+    os.sched_setaffinity(0, {core})
+    try:
+        t0 = time.perf_counter()
+        lg = O.loss_grad(op, t, rows=rows)
+        t1 = time.perf_counter()
+        opt = O.Adam(op.K, op.Pk)
+        opt.step(op, lg.grad, O.LR())
+        t2 = time.perf_counter()
+    finally:
+        os.sched_setaffinity(0, old)
+    return t1 - t0, t2 - t1, core
 
 
 def run_reference(args):
@@ -121,7 +144,7 @@ def run_reference(args):
     times = []
     for i in range(args.warmup + args.steps):
         r0 = (i * 97) % (H - rows_per_step + 1)
-        tg, ta = cpu_oracle_sample(target, pool, (r0, r0 + rows_per_step))
+        tg, ta, core = cpu_oracle_sample(target, pool, (r0, r0 + rows_per_step))
         if i >= args.warmup:
             times.append((tg, ta))
     tg = sum(t[0] for t in times) / len(times)
@@ -136,7 +159,8 @@ def run_reference(args):
         "ms_per_step": sec_per_iter * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_dict(args.config, world),
-        "cpu_baseline": {"value": value, "unit": "it/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": dict({"value": value, "unit": "it/s", "cores": 1, "kind": "oracle", "sample": sample,
+                              "pinned_core": core}, **cpu_info()),
         "e2e": {"value": value, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out))
@@ -235,14 +259,14 @@ def e2e_banded(fit, params, target, T_total, steps, dev):
     from paper_2510_05814_b200 import smoe
     host_t = torch.as_tensor(target).pin_memory()
     n = min(steps, 500)
-    ring = torch.empty((4, 3), dtype=torch.float64).pin_memory()
+    ring = torch.empty((4, 4), dtype=torch.float64).pin_memory()
     evs = [torch.cuda.Event() for _ in range(4)]
     lag, losses = 2, []
     torch.cuda.synchronize()
     dist.barrier()
     t0 = time.perf_counter()
     for i in range(n):
-        sums = fit.step(params, host_t, smoe.LR.paper(T_total, T_total), stats=True)
+        sums = fit.step(params, host_t, smoe.LR.paper(T_total, T_total))
         ring[i % 4].copy_(sums, non_blocking=True)
         evs[i % 4].record()
         if i >= lag:
@@ -256,9 +280,10 @@ def e2e_banded(fit, params, target, T_total, steps, dev):
     assert len(losses) == n and all(np.isfinite(losses))
     r0, r1 = fit.band
     return {"value": n / float(dt.item()), "unit": "it/s", "h2d_bytes_per_step": int(target.nbytes),
-            "d2h_bytes_per_step": 24 * fit.world, "steps": n,
-            "note": "each rank: pinned H2D of its band's target rows (double-buffered copy stream), gradient + "
-                    "loss all-reduce, async D2H of the reduced loss partials; bytes summed over ranks, time max over ranks"}
+            "d2h_bytes_per_step": 32 * fit.world, "steps": n,
+            "note": "each rank: pinned H2D of its band's target rows (double-buffered copy stream), gradient reduce-scatter + "
+                    "loss all-reduce + sharded Adam + parameter all-gather, async D2H of the reduced loss partials; "
+                    "bytes summed over ranks, time max over ranks"}
 
 
 def main():
@@ -267,7 +292,7 @@ def main():
     ap.add_argument("--steps", type=int, default=2000)   # the config's 2000-iteration fit
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="kodak", choices=["tiny", "kodak", "div2k", "denoise", "8k"])
+    ap.add_argument("--config", default="div2k", choices=["tiny", "kodak", "div2k", "denoise", "8k"])
     ap.add_argument("--cpu-rows", type=int, default=64, help="image rows of the cpu_baseline sample")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -292,7 +317,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2510_05814_b200 import smoe, synth
-    from paper_2510_05814_b200.dist import BandedFit
+    from paper_2510_05814_b200.dist import BandedFit, padded
 
     rank, world, local = rank_env()
     local = local % torch.cuda.device_count()       # ranks may share a GPU under --dist-backend gloo
@@ -310,19 +335,26 @@ def main():
     dev = torch.device("cuda", local)
     tgt = torch.as_tensor(target).to(dev)
     params = smoe.Params.from_numpy(pool, dev)
+    if world > 1:
+        params = padded(params, world)       # in-place parameter all-gather needs Kpad rows
     h = smoe.SMoE(K, H, W, C, order, device=local, backward_mode=args.backward_mode)
     fit = BandedFit(h, rank, world) if world > 1 else None
-    T_total = args.warmup + args.steps
+    # the learning-rate schedule spans the config's fit; the timed
+    # steps are its first ones, the rest of the fit runs untimed before the
+    # render so the render is timed on the fitted model
+    T_total = max(args.warmup + args.steps, cfg["iters"])
 
     def step(t):
         lr = smoe.LR.paper(t, T_total)
         if fit is None:
             h.step(params, tgt, lr, stats=False)
         else:
-            fit.step(params, tgt, lr, stats=False)
+            fit.step(params, tgt, lr)
 
     flush = None if args.no_flush else L2Flush(dev)
     st0 = h.step(params.clone(), tgt, smoe.LR(0, 0, 0, 0, 0), stats=True)   # calibrate capacity
+    if world > 1:
+        h.grad(params, tgt)                  # calibrate the band's own lists
     h.reset_adam()
     for t in range(args.warmup):
         step(t)
@@ -354,7 +386,9 @@ def main():
     # second timed region, same steps: CUDA event pairs (graph event nodes on
     # the launch stream) around the dominant kernel, for its roofline; kept
     # out of the headline region because event nodes cost ~10 us per step
+    t_last = args.warmup + args.steps - 1
     ktimes, tested, hits, n_prof = {}, 0, 0, 0
+    sort_cycles = cta_cycles = 0
     if not args.no_profile:
         n_prof = min(args.steps, 200)
         h.profile_begin(n_prof + 16, kernels=["k_raster<train>"])
@@ -362,7 +396,7 @@ def main():
         for i in range(n_prof):
             if flush is not None:
                 flush()
-            step(T_total - 1)
+            step(t_last)
         ktimes, _ = h.profile_end()
 
     st = h.sync()
@@ -379,17 +413,46 @@ def main():
         for i in range(nb):
             if flush is not None:
                 flush()
-            step(T_total - 1)
+            step(t_last)
         bt, (tested, hits) = h.profile_end()
+        sort_cycles, cta_cycles = h.last_work[2], h.last_work[3]
         breakdown = {k: v[0] / nb for k, v in bt.items()}
         tested, hits = tested / nb, hits / nb        # per raster launch
+
+    # the rest of the config's fit, untimed (the render below is timed on the
+    # fitted model)
+    for t in range(args.warmup + args.steps, T_total):
+        step(t)
+    st_fit = h.sync()
 
     # roofline of the dominant kernel (raster: FP32 pipe)
     peaks, peak_kind = load_peaks()
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
     a_t, a_h = ops_per_unit(C, order)
     roof = None
+    kernels = {}
     rast = ktimes.get("k_raster<train>")
+    if breakdown:
+        # per-kernel rooflines: the raster against the FP32
+        # lanes and the MUFU (ex2: one per hit pair forward, one backward;
+        # 16 MUFU lanes per SM per clock), binning and Adam against HBM
+        # with their algorithmic bytes per launch
+        E = 1 + 2 * order
+        Pk, RSb = 6 + C * E, ((6 + C * E + 3) // 4) * 16
+        V = 8 if Pk <= 8 else 16
+        hbm = peaks.get("hbm_gbs", 6554.2)
+        pairs = st.pairs
+        pre_bytes = K * (4 * Pk + 16 + RSb) + 4 * pairs
+        adam_bytes = K * (24 * Pk + 8 * V)
+        for name, b, what in (("k_preprocess", pre_bytes, f"read params {4 * Pk} B + write tile box 16 B + record "
+                                                        f"{RSb} B per kernel, + 4 B kernel id per pair (count "
+                                                        f"atomics are L2 traffic, not counted)"),
+                              ("k_adam", adam_bytes, f"per kernel: params, m1, m2 read + write ({24 * Pk} B), raw "
+                                                     f"sums read + zeroed ({8 * V} B)")):
+            if name in breakdown and breakdown[name] > 0:
+                gbs = b / (breakdown[name] * 1e-3) / 1e9
+                kernels[name] = {"bound": "hbm", "bytes_per_launch": b, "avg_ms": breakdown[name],
+                                 "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm, "bytes_note": what}
     if rast:
         r_ms, r_n = rast
         ops = a_t * tested + a_h * hits          # per launch (counted in the breakdown pass)
@@ -409,6 +472,14 @@ def main():
                 "tested_pairs_per_launch": tested, "hit_pairs_per_launch": hits,
                 "avg_ms": r_ms / r_n, "share_of_step": (r_ms / r_n) / ms_step if world == 1 else None,
                 "timed_region": f"second pass of {n_prof} steps with event pairs around the raster"}
+        mufu_peak = 148 * 16 * sm_mhz * 1e6 / 1e12
+        mufu = 2 * hits / (r_ms / r_n * 1e-3) / 1e12
+        kernels["k_raster<train>"] = {
+            "bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "mufu": {"achieved": mufu, "peak": mufu_peak, "unit": "Tex2/s", "frac": mufu / mufu_peak,
+                     "note": "ex2 per hit pair: 1 forward + 1 backward; peak 16 MUFU lanes/SM/clk"},
+            "sort_share": (sort_cycles / cta_cycles) if cta_cycles else None,
+            "sort_note": "a4 in-raster bucket sort: SM cycles of the raster CTAs spent sorting / all their cycles"}
 
     # render (a9): plain reconstruction and the config's SR factor
     render = {}
@@ -479,10 +550,11 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         rows = min(args.cpu_rows, H)
         r0 = (H - rows) // 2
-        tg, ta = cpu_oracle_sample(target, pool, (r0, r0 + rows))
-        cpu = {"value": 1.0 / (tg * H / rows + ta), "unit": "it/s", "cores": 1, "kind": "oracle",
-               "sample": f"dense fp64 loss+gradient on image rows {r0}-{r0 + rows} of {H} ({rows * W} px x "
-                         f"{K} kernels, {tg:.1f} s) + full Adam ({ta:.3f} s), extrapolated to one iteration"}
+        tg, ta, core = cpu_oracle_sample(target, pool, (r0, r0 + rows))
+        cpu = dict({"value": 1.0 / (tg * H / rows + ta), "unit": "it/s", "cores": 1, "kind": "oracle",
+                    "sample": f"dense fp64 loss+gradient on image rows {r0}-{r0 + rows} of {H} ({rows * W} px x "
+                              f"{K} kernels, {tg:.1f} s) + full Adam ({ta:.3f} s), extrapolated to one iteration",
+                    "pinned_core": core}, **cpu_info())
 
     if rank == 0:
         out = {
@@ -490,11 +562,13 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": dict(config_dict(args.config, world), **({"K": K, "K_override": True} if args.K else {})),
-            "render": render, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "render": render, "roofline": roof, "kernel_rooflines": kernels, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk,
             "kernel_ms_per_step": breakdown,
             "fit_stats": {"pairs": st.pairs, "avg_kernels_per_block": st.pairs / max(st.n_tiles, 1),
-                          "loss": st.loss, "psnr_db": st.psnr_db, "initial_psnr_db": st0.psnr_db},
+                          "loss": st.loss, "psnr_db": st.psnr_db, "initial_psnr_db": st0.psnr_db,
+                          "fit_iterations_before_render": T_total,
+                          "final_pairs": st_fit.pairs, "final_psnr_db": st_fit.psnr_db},
         }
         print(json.dumps(out))
     if world > 1:

@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define SMOE_ABI_VERSION 1
+#define SMOE_ABI_VERSION 2
 
 typedef struct smoe_ctx *smoe_handle;
 
@@ -167,16 +167,35 @@ smoe_status smoe_set_band(smoe_handle h, int tile_row0, int tile_row1);
 
 /* Gradient of the loss restricted to the current band: grad[K][Pk] float32
  * with Pk = 6 + C E, per kernel (mu_x, mu_y, l11, l21, l22, log_pi, expert
- * block in the expert layout); sums[3] float64 = (SSE, clamped SSE, uncovered
- * pixels) of the band.  grad and sums may be host or device pointers.
+ * block in the expert layout); sums[4] float64 = (SSE, clamped SSE, uncovered
+ * pixels, skipped) of the band.  grad and sums may be host or device pointers.
  * target[C][H][W] is the full image; a host target has only the band's
- * pixel rows copied to the device (the other rows are never read). */
+ * pixel rows copied to the device (the other rows are never read).
+ * Capacity: with grad and sums both on the device the call is asynchronous;
+ * if the band's block lists overflowed their capacity the raster is skipped,
+ * grad is written as zeros and sums = (0, 0, 0, 1): the caller must not apply
+ * that gradient (smoe_apply_ex with `sums` does the check on the device) and
+ * the next synchronising call (smoe_sync) grows the lists and returns
+ * SMOE_ERR_CAPACITY.  With a host grad or sums the call synchronises, grows
+ * and redoes the pass itself (sums[3] = 0). */
 smoe_status smoe_grad(smoe_handle h, const smoe_params *p, const float *target,
                       float *grad, double *sums);
 
 /* Adam update with a caller-supplied gradient (e.g. all-reduced over ranks):
  * same update and clamp as smoe_step.  grad[K][Pk] host or device. */
 smoe_status smoe_apply(smoe_handle h, smoe_params *p, const float *grad, const smoe_lr *lr);
+
+/* Sharded Adam update (multi-GPU reduce-scatter -> per-rank update ->
+ * all-gather): updates kernels [k0, k1) only, with
+ * grad[(k1-k0)][Pk] (rows relative to k0; host or device) and the Adam
+ * moments of those kernels; parameters of other kernels are untouched.
+ * `sums` (NULL, or the all-reduced sums[4] of smoe_grad, host or device):
+ * if sums[3] != 0 some rank's binning overflowed and no parameter is updated
+ * (checked on the device for a device pointer, so the call stays
+ * asynchronous).  0 <= k0 <= k1 <= K.  The Adam step counter advances when
+ * k1 > k0 and the update is not skipped. */
+smoe_status smoe_apply_ex(smoe_handle h, smoe_params *p, const float *grad, const smoe_lr *lr, int k0, int k1,
+                          const double *sums);
 
 /* Zero the Adam moments and the step counter. */
 smoe_status smoe_reset_adam(smoe_handle h);
@@ -234,7 +253,9 @@ enum {
     SMOE_KERNEL_RASTER_TRAIN = 2,  /* a4 (bucket sort) + a5-a7               */
     SMOE_KERNEL_RASTER_RENDER = 3, /* a4 + a5/a9                             */
     SMOE_KERNEL_ADAM = 4,          /* a8                                     */
-    SMOE_KERNEL_COUNT = 5
+    SMOE_KERNEL_BIN = 5,           /* a1-a3 fused cooperative binner (CSR)   */
+    SMOE_KERNEL_SCAN = 6,          /* a2 decoupled look-back scan (CSR)      */
+    SMOE_KERNEL_COUNT = 7
 };
 #define SMOE_PROFILE_COUNT_WORK 0x80000000u
 typedef struct {
@@ -244,6 +265,9 @@ typedef struct {
 typedef struct {
     long long tested_pairs;   /* valid pixel x listed kernel, forward sweep */
     long long hit_pairs;      /* of those, d^2 <= R2                        */
+    long long sort_cycles;    /* SM cycles the raster CTAs spent in the a4
+                                 bucket sort (summed over CTAs)             */
+    long long cta_cycles;     /* SM cycles of the raster CTAs in total      */
 } smoe_work;
 smoe_status smoe_profile_begin(smoe_handle h, int max_launches, unsigned kernel_mask);
 smoe_status smoe_profile_end(smoe_handle h, smoe_kernel_time *times, smoe_work *work);
@@ -261,7 +285,9 @@ const char *smoe_kernel_name(int id);
  * each plus largest-remainder top-up to exactly K (Eq. 9: |B_j| ~ |R_j|/n_k);
  * centres uniform over the segment's pixels, L = (scale_px, 0, scale_px),
  * log_pi = 0, expert = segment mean colour, slopes 0.  Outputs are HOST
- * arrays in the smoe_params layout.  K < N gives SMOE_ERR_INVALID_ARG. */
+ * arrays in the smoe_params layout.  K < N, H < 1, W < 1, a label outside
+ * [0, N) or a segment id in [0, N) that owns no pixel give
+ * SMOE_ERR_INVALID_ARG. */
 smoe_status smoe_segment(const float *image, int H, int W, int C, float threshold, int min_size, int *labels,
                          int *n_segments);
 smoe_status smoe_segment_init(const float *image, int H, int W, int C, const int *labels, int n_segments, int K,

@@ -70,6 +70,8 @@ def _lib():
         lib.oracle_grad_kernels.argtypes = [I, I, I, P, P, P, P, I, I, P, D, I, P, P, P]
         lib.oracle_margins.restype = None
         lib.oracle_margins.argtypes = [I, P, P, D, I, I, I, I, P, P]
+        lib.oracle_point_margins.restype = None
+        lib.oracle_point_margins.argtypes = [I, P, P, D, I, P, P, P]
         lib.oracle_set_head.restype = None
         lib.oracle_set_head.argtypes = [I]
         _LIB = lib
@@ -322,6 +324,17 @@ def margins(p: Params, H, W, out_H=None, out_W=None, R2=None):
     eg = np.zeros(p.K)
     _lib().oracle_margins(p.K, _ptr(mu), _ptr(ch), R2, H, W, out_H, out_W, _ptr(dg), _ptr(eg))
     return dg, eg
+
+
+def point_margins(p: Params, xs, ys, R2=None):
+    """Per source-space point: min over every kernel of |d^2 - R2| (dense);
+    used to keep sampled parity away from the cull discontinuity."""
+    R2 = R2_99() if R2 is None else R2
+    xs, ys = _f64(xs).ravel(), _f64(ys).ravel()
+    mu, ch, _, _ = _args(p)
+    gap = np.zeros(xs.size)
+    _lib().oracle_point_margins(p.K, _ptr(mu), _ptr(ch), R2, xs.size, _ptr(xs), _ptr(ys), _ptr(gap))
+    return gap
 
 
 # ---------------------------------------------------------------- metrics ---

@@ -378,3 +378,23 @@ void oracle_margins(int K, const double *mu, const double *chol, double R2,
         d2_gap[k] = dg;
     }
 }
+
+/* Margin of sample points for sampled parity (SURVEY §8(c) rule P1 applied
+ * to samples instead of kernels): for each point x_i, the smallest
+ * |d^2_j(x_i) - R2| over EVERY kernel j (dense).  A pixel whose value could
+ * depend on a cull decision taken differently in fp32 and fp64 has a small
+ * margin; a pixel with margin tau in d^2 is also inside every listing box
+ * by at least r tau / (2 R2) px, so box-edge rounding cannot drop a kernel
+ * it needs. */
+void oracle_point_margins(int K, const double *mu, const double *chol, double R2,
+                          int n, const double *xs, const double *ys, double *gap)
+{
+    for (int i = 0; i < n; i++) {
+        double g = 1e300;
+        for (int k = 0; k < K; k++) {
+            double d = fabs(oracle_d2(mu + 2 * k, chol + 3 * k, xs[i], ys[i]) - R2);
+            if (d < g) g = d;
+        }
+        gap[i] = g;
+    }
+}

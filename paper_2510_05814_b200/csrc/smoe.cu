@@ -57,7 +57,7 @@ struct Prof {
 // Arguments of one k_adam launch, kept so a captured graph's Adam node can
 // be re-parameterised (new learning rates) before every replay.
 struct AdamArgs {
-    int K;
+    AdamCommon cm;
     ParamsMut pm;
     float *acc;
     const float *gin;
@@ -70,7 +70,7 @@ struct AdamArgs {
     void *ptrs[11];
     void bind()
     {
-        void *a[11] = {&K, &pm, &acc, &gin, &gout, &m1, &m2, &lr, &hc, &gc, &cap};
+        void *a[11] = {&cm, &pm, &acc, &gin, &gout, &m1, &m2, &lr, &hc, &gc, &cap};
         for (int i = 0; i < 11; i++) ptrs[i] = a[i];
     }
 };
@@ -418,7 +418,7 @@ void bin_unfused(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_h
     }
     if (g.lb_state) {
         int nb2 = (g.n_tiles + LB_CHUNK - 1) / LB_CHUNK;
-        launch(h, SMOE_KERNEL_PREPROCESS, "k_scan_lookback", [&] {
+        launch(h, SMOE_KERNEL_SCAN, "k_scan_lookback", [&] {
             k_scan_lookback<<<nb2, LB_NT, 0, h->stream>>>(g.cnt, g.n_tiles, g.start, g.cursor, g.cap, g.gc,
                                                            zero_stats ? h->ctl->dstats : nullptr, g.lb_state);
         });
@@ -466,7 +466,7 @@ void bin(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_hi, bool 
     B.order = SMOE_LPT && !getenv("SMOE_NO_LPT") ? g.order : nullptr;
     B.chunk = g.chunk; B.hist = g.hist; B.cap = g.cap; B.gc = g.gc; B.hc = &h->ctl->hc;
     B.dstats = zero_stats ? h->ctl->dstats : nullptr;
-    launch(h, SMOE_KERNEL_PREPROCESS, "k_bin", [&] {
+    launch(h, SMOE_KERNEL_BIN, "k_bin", [&] {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(g.bin_grid);
         cfg.blockDim = dim3(BIN_NT);
@@ -605,9 +605,13 @@ void *adam_func(smoe_ctx *h, int mode)
 }
 
 void adam_args(smoe_ctx *h, const smoe_params *p, const float *grad_in, float *grad_out, const smoe_lr *lr,
-               AdamArgs &a)
+               AdamArgs &a, int k0 = 0, int n = -1, const double *skip_in = nullptr)
 {
-    a.K = h->K;
+    a.cm.Ktot = h->K;
+    a.cm.k0 = k0;
+    a.cm.n = n < 0 ? h->K : n;
+    a.cm.skip_in = skip_in;
+    a.cm.dstats = h->ctl->dstats;
     a.pm = ParamsMut{p->mu, p->chol, p->log_pi, p->expert};
     a.acc = h->acc;
     a.gin = grad_in;
@@ -622,19 +626,20 @@ void adam_args(smoe_ctx *h, const smoe_params *p, const float *grad_in, float *g
 }
 
 void launch_adam(smoe_ctx *h, int mode, const smoe_params *p, const float *grad_in, float *grad_out,
-                 const smoe_lr *lr)
+                 const smoe_lr *lr, int k0 = 0, int n = -1, const double *skip_in = nullptr)
 {
     AdamArgs a;
-    adam_args(h, p, grad_in, grad_out, lr, a);
+    adam_args(h, p, grad_in, grad_out, lr, a, k0, n, skip_in);
     void *f = adam_func(h, mode);
     dim3 grid, block;
+    const int cnt = std::max(1, a.cm.n);
     if (adam_elementwise(h)) {
         int kpb = 0;
         DISPATCH_CE(h, (kpb = ADAM_NT / Rec<C_, E_>::V));
-        grid = dim3((h->K + kpb - 1) / kpb);
+        grid = dim3((cnt + kpb - 1) / kpb);
         block = dim3(ADAM_NT);
     } else {
-        grid = dim3((h->K + 63) / 64);
+        grid = dim3((cnt + 63) / 64);
         block = dim3(64);
     }
     launch(h, SMOE_KERNEL_ADAM, "k_adam", [&] {
@@ -1036,7 +1041,7 @@ smoe_status smoe_grad(smoe_handle h, const smoe_params *p, const float *target, 
             run_sequence(h, 1, p, t, gout, nullptr);
             if (gdev && sdev) {
                 if (sums)
-                    CK(cudaMemcpyAsync(sums, h->ctl->dstats, 3 * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+                    CK(cudaMemcpyAsync(sums, h->ctl->dstats, 4 * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
                 return SMOE_OK;
             }
             read_ctl(h);
@@ -1047,8 +1052,8 @@ smoe_status smoe_grad(smoe_handle h, const smoe_params *p, const float *target, 
                 CK(cudaStreamSynchronize(h->stream));
             }
             if (sums) {
-                if (sdev) CK(cudaMemcpy(sums, h->ctl->dstats, 3 * sizeof(double), cudaMemcpyDeviceToDevice));
-                else std::memcpy(sums, h->h_ctl->dstats, 3 * sizeof(double));
+                if (sdev) CK(cudaMemcpy(sums, h->ctl->dstats, 4 * sizeof(double), cudaMemcpyDeviceToDevice));
+                else std::memcpy(sums, h->h_ctl->dstats, 4 * sizeof(double));
             }
             return st;
         }
@@ -1058,17 +1063,34 @@ smoe_status smoe_grad(smoe_handle h, const smoe_params *p, const float *target, 
 smoe_status smoe_apply(smoe_handle h, smoe_params *p, const float *grad, const smoe_lr *lr)
 {
     if (!h) return SMOE_ERR_BAD_HANDLE;
+    return smoe_apply_ex(h, p, grad, lr, 0, h->K, nullptr);
+}
+
+smoe_status smoe_apply_ex(smoe_handle h, smoe_params *p, const float *grad, const smoe_lr *lr, int k0, int k1,
+                          const double *sums)
+{
+    if (!h) return SMOE_ERR_BAD_HANDLE;
     return guard(h, [&]() -> smoe_status {
         check_params(p);
         if (!grad || !lr) throw SmoeError(SMOE_ERR_INVALID_ARG, "smoe_apply: NULL grad or lr");
+        if (k0 < 0 || k1 > h->K || k0 > k1) throw SmoeError(SMOE_ERR_INVALID_ARG, "smoe_apply_ex: need 0 <= k0 <= k1 <= K");
+        const double *skip = nullptr;
+        if (sums) {
+            if (is_device_ptr(sums)) {
+                skip = sums + 3;
+            } else if (sums[3] != 0.0) {
+                return SMOE_OK;   // a rank skipped its band: no update anywhere
+            }
+        }
+        if (k1 == k0) return SMOE_OK;
         const float *g = grad;
+        size_t n = (size_t)(k1 - k0) * h->P;
         if (!is_device_ptr(grad)) {
-            size_t n = (size_t)h->K * h->P;
             float *d = stage(h->stage_in, h->stage_in_n, n);
             CK(cudaMemcpyAsync(d, grad, n * sizeof(float), cudaMemcpyHostToDevice, h->stream));
             g = d;
         }
-        launch_adam(h, 2, p, g, nullptr, lr);
+        launch_adam(h, 2, p, g, nullptr, lr, k0, k1 - k0, skip);
         return SMOE_OK;
     });
 }
@@ -1257,7 +1279,7 @@ smoe_status smoe_stats_from_raw(smoe_handle h, const smoe_raw_stats *raw, smoe_s
 const char *smoe_kernel_name(int id)
 {
     static const char *names[SMOE_KERNEL_COUNT] = {"k_preprocess", "k_scatter", "k_raster<train>",
-                                                   "k_raster<render>", "k_adam"};
+                                                   "k_raster<render>", "k_adam", "k_bin", "k_scan_lookback"};
     return (id >= 0 && id < SMOE_KERNEL_COUNT) ? names[id] : "?";
 }
 
@@ -1276,8 +1298,8 @@ smoe_status smoe_profile_begin(smoe_handle h, int max_launches, unsigned kernel_
         P.max = max_launches;
         P.n = 0;
         P.mask = kernel_mask ? kernel_mask : 0xffffffffu;
-        if (!P.d_work) CK(cudaMalloc(&P.d_work, 2 * sizeof(unsigned long long)));
-        CK(cudaMemsetAsync(P.d_work, 0, 2 * sizeof(unsigned long long), h->stream));
+        if (!P.d_work) CK(cudaMalloc(&P.d_work, 4 * sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(P.d_work, 0, 4 * sizeof(unsigned long long), h->stream));
         P.on = true;
         return SMOE_OK;
     });
@@ -1299,10 +1321,12 @@ smoe_status smoe_profile_end(smoe_handle h, smoe_kernel_time *times, smoe_work *
             }
         }
         if (work) {
-            unsigned long long w[2] = {0, 0};
+            unsigned long long w[4] = {0, 0, 0, 0};
             if (P.d_work) CK(cudaMemcpy(w, P.d_work, sizeof(w), cudaMemcpyDeviceToHost));
             work->tested_pairs = (long long)w[0];
             work->hit_pairs = (long long)w[1];
+            work->sort_cycles = (long long)w[2];
+            work->cta_cycles = (long long)w[3];
         }
         P.on = false;
         P.n = 0;

@@ -230,9 +230,6 @@ preprocess_one(int k, ParamsDev p, float R2, float sx, float sy, int oW, int oH,
     }
 #pragma unroll
     for (int i = R::P; i < R::RS; i++) r[i] = 0.0f;
-    float4 *dst = reinterpret_cast<float4 *>(rec) + (size_t)k * (R::RS / 4);
-#pragma unroll
-    for (int q = 0; q < R::RS / 4; q++) dst[q] = make_float4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
     if (!ok) atomicExch((unsigned long long *)&hc->nonfinite, 1ull);
 
     float s11 = l11 * l11, s12 = l11 * l21, s22 = l21 * l21 + l22 * l22;
@@ -249,6 +246,14 @@ preprocess_one(int k, ParamsDev p, float R2, float sx, float sy, int oW, int oH,
     if (ok && xl <= xh && yl <= yh) {
         tb = make_int4((int)xl / TILE, (int)xh / TILE, (int)yl / TILE, (int)yh / TILE);
         int y0 = max(tb.z, ty_lo), y1 = min(tb.w, ty_hi - 1);
+        // the record is read only through the block lists: write it only for
+        // a kernel listed in some block of the band (a multi-GPU rank skips
+        // the records of kernels outside its band)
+        if (y0 <= y1) {
+            float4 *dst = reinterpret_cast<float4 *>(rec) + (size_t)k * (R::RS / 4);
+#pragma unroll
+            for (int q = 0; q < R::RS / 4; q++) dst[q] = make_float4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+        }
         if (direct) {
             // direct buckets: the count atomic returns k's slot in block t's
             // fixed-capacity bucket (PRE_ATOM atomics in flight per round)
@@ -861,7 +866,8 @@ struct RasterArgs {
     // render
     float *out;           // [C][oH][oW]
     float accum;          // 0: out = y; else out += accum * y
-    // profiling (PROF instantiation only): tested / hit (pixel, kernel) pairs
+    // profiling (PROF instantiation only): tested / hit (pixel, kernel)
+    // pairs, SM cycles in the bucket sort, SM cycles of the whole CTA
     unsigned long long *work;
 };
 
@@ -945,16 +951,23 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
     // direct buckets: the count is consumed here and reset for the next
     // binning (when n > 0 every thread has read it before thread 0 passes the
     // first batch barrier, and thread 0 resets it only at its return)
+    // PROF: SM cycles of this CTA in the bucket sort (a4) and in total
+    const long long c_start = PROF ? clock64() : 0;
     auto release = [&] {
         if (A.len && threadIdx.x == 0) {
             A.lenout[tile] = n;
             if (n) A.len[tile] = 0;
         }
+        if (PROF && threadIdx.x == 0) atomicAdd(&A.work[3], (unsigned long long)(clock64() - c_start));
     };
     // a4 (second digit): sort this block's bucket by kernel id; srec doubles
     // as the shared scratch (its capacity in ints is a power of two >= 1024)
     constexpr int SCHUNK = (BATCH * RS4 * 4 >= 2048) ? 2048 : 1024;
     sort_bucket(A.ids + s0, n, A.tmp + s0, reinterpret_cast<int *>(srec), SCHUNK);
+    if (PROF) {
+        __syncthreads();
+        if (threadIdx.x == 0) atomicAdd(&A.work[2], (unsigned long long)(clock64() - c_start));
+    }
 
     float2 D2 = make_float2(0.f, 0.f), N2[C];
 #pragma unroll
@@ -1221,7 +1234,9 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
         if (lo < hi) {
             // the record holding entry lo: last record with prefix <= lo
             int ra = 0;
-            for (int step = 64; step >= 1; step >>= 1)
+            static_assert(BATCH >= 2 && BATCH <= 1024 && (BATCH & (BATCH - 1)) == 0,
+                          "record search: BATCH must be a power of two");
+            for (int step = BATCH / 2; step >= 1; step >>= 1)
                 if (ra + step < nr && (int)skr[warp][ra + step].w <= lo) ra += step;
             uint4 kr = skr[warp][ra];
             unsigned m = kr.x | kr.y;
@@ -1352,6 +1367,18 @@ k_raster(RasterArgs A)
     const int tile = A.order ? A.order[i] : A.tile0 + i;
     if (A.gc->skip) {   // overflowed binning: no work, but the counts are reset
         if (A.len && threadIdx.x == 0) A.len[tile] = 0;
+        if (!TRAIN && A.out) {
+            // a skipped render leaves NaN in its output (accumulate: NaN is
+            // added), never stale memory; the host reports SMOE_ERR_CAPACITY
+            // at the next synchronising call and grows the lists
+            const int tx = tile % A.nx, ty = tile / A.nx;
+            const size_t plane = (size_t)A.oH * A.oW;
+            for (int i = threadIdx.x; i < TILE * TILE; i += blockDim.x) {
+                const int x = tx * TILE + (i & (TILE - 1)), y = ty * TILE + i / TILE;
+                if (x < A.oW && y < A.oH)
+                    for (int c = 0; c < C; c++) A.out[c * plane + (size_t)y * A.oW + x] = __int_as_float(0x7fc00000);
+            }
+        }
         return;
     }
     raster_tile<C, E, TRAIN, PROF, KPAR>(A, tile);
@@ -1394,9 +1421,36 @@ __device__ __forceinline__ float *param_slot(const ParamsMut &p, int k, int v)
 // parameters are staged in shared memory (the chain rule of element v needs
 // several of its kernel's sums and its Cholesky factor); moments and the
 // update run parameter-major.
+// Common arguments of the Adam kernels.  Kernels [k0, k0 + n) of the pool of
+// Ktot are processed (MODE 2 on a multi-GPU kernel shard; k0 = 0, n = Ktot
+// otherwise); grad_in / grad_out are [n][P] (rows relative to k0), the
+// moments [P][Ktot] and the parameters absolute.
+struct AdamCommon {
+    int Ktot, k0, n;
+    const double *skip_in;   // MODE 2: all-reduced skip flag (sums[3]); non-zero = no update
+    double *dstats;          // MODE 0/1: dstats[3] = 1 when the binning overflowed
+};
+
+// An overflowed binning skipped the raster: MODE 1 writes a zero gradient
+// (never stale memory) and both modes flag the skip in dstats[3], which
+// smoe_grad returns as sums[3] (multi-GPU ranks all-reduce it and skip the
+// update together).  Returns true when the caller must return.
+template <int P, int MODE>
+__device__ __forceinline__ bool adam_skipped(const AdamCommon &cm, float *grad_out, const GridCtr *gc)
+{
+    if (MODE == 2) return cm.skip_in && *cm.skip_in != 0.0;
+    if (!gc->skip) return false;
+    if (MODE == 1)
+        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < (long long)cm.n * P;
+             i += (long long)gridDim.x * blockDim.x)
+            grad_out[i] = 0.f;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && cm.dstats) cm.dstats[3] = 1.0;
+    return true;
+}
+
 template <int C, int E, int MODE>
 __global__ void __launch_bounds__(ADAM_NT)
-k_adam(int K, ParamsMut p, float *__restrict__ acc, const float *__restrict__ grad_in,
+k_adam(AdamCommon cm, ParamsMut p, float *__restrict__ acc, const float *__restrict__ grad_in,
        float *__restrict__ grad_out, float *__restrict__ m1, float *__restrict__ m2,
        LrDev lr, HandleCtr *hc, const GridCtr *gc, long long cap)
 {
@@ -1404,7 +1458,8 @@ k_adam(int K, ParamsMut p, float *__restrict__ acc, const float *__restrict__ gr
     constexpr int P = R::P, V = R::V, KPB = ADAM_NT / V, KPC = ADAM_IT * KPB;
     __shared__ float s_raw[KPC][V + 1];
     __shared__ float s_prm[KPC][V + 1];
-    if (MODE != 2 && gc->skip) return;
+    if (adam_skipped<P, MODE>(cm, grad_out, gc)) return;
+    const int K = cm.Ktot, k0r = cm.k0, kend = cm.k0 + cm.n;
     const long long t = hc->t + 1;
     // 1 - beta^t = -expm1(t log(beta)), accurate to a few ulp for every t
     const float bc1 = MODE == 1 ? 1.f : -expm1f((float)t * log1pf(-0.1f));
@@ -1413,9 +1468,9 @@ k_adam(int K, ParamsMut p, float *__restrict__ acc, const float *__restrict__ gr
     bool bad = false;
     // grid-stride over chunks of KPC kernels (the host launches one CTA per
     // chunk; the loop only guards other grid sizes)
-    const int nchunk = (K + KPC - 1) / KPC;
+    const int nchunk = (cm.n + KPC - 1) / KPC;
     for (int chunk = blockIdx.x; chunk < nchunk; chunk += gridDim.x) {
-        const int k0 = chunk * KPC;
+        const int k0 = k0r + chunk * KPC;
         // every load is issued before any use: kernel-major (thread = kernel
         // kl, slot v; acc[k0*V + ...] is contiguous) for the raw sums and
         // parameters, parameter-major for the moments
@@ -1425,17 +1480,17 @@ k_adam(int K, ParamsMut p, float *__restrict__ acc, const float *__restrict__ gr
 #pragma unroll
         for (int it = 0; it < ADAM_IT; it++) {
             const int k = k0 + it * KPB + threadIdx.x % KPB;
-            const bool live = v < P && k < K;
+            const bool live = v < P && k < kend;
             a1[it] = a2[it] = gi[it] = 0.f;
             if (live && MODE != 1) { a1[it] = m1[(size_t)v * K + k]; a2[it] = m2[(size_t)v * K + k]; }
-            if (live && MODE == 2) gi[it] = grad_in[(size_t)k * P + v];
+            if (live && MODE == 2) gi[it] = grad_in[(size_t)(k - k0r) * P + v];
         }
         float rv[ADAM_IT], pv[ADAM_IT];
 #pragma unroll
         for (int it = 0; it < ADAM_IT; it++) {
             const int kl = it * KPB + (int)threadIdx.x / V, v = threadIdx.x % V, k = k0 + kl;
             rv[it] = pv[it] = 0.f;
-            if (k < K) {
+            if (k < kend) {
                 if (MODE != 2) rv[it] = acc[(size_t)k0 * V + it * ADAM_NT + threadIdx.x];
                 pv[it] = *param_slot<C, E>(p, k, min(v, P - 1));
             }
@@ -1450,12 +1505,12 @@ k_adam(int K, ParamsMut p, float *__restrict__ acc, const float *__restrict__ gr
         if (MODE != 2) {
 #pragma unroll
             for (int it = 0; it < ADAM_IT; it++)
-                if (k0 + it * KPB + (int)threadIdx.x / V < K) acc[(size_t)k0 * V + it * ADAM_NT + threadIdx.x] = 0.f;
+                if (k0 + it * KPB + (int)threadIdx.x / V < kend) acc[(size_t)k0 * V + it * ADAM_NT + threadIdx.x] = 0.f;
         }
 #pragma unroll
         for (int it = 0; it < ADAM_IT; it++) {
             const int kl = it * KPB + threadIdx.x % KPB, k = k0 + kl;
-            if (!(v < P && k < K)) continue;
+            if (!(v < P && k < kend)) continue;
             const float *raw = s_raw[kl], *prm = s_prm[kl];
             float g = gi[it];
             if (MODE != 2) {
@@ -1485,7 +1540,7 @@ k_adam(int K, ParamsMut p, float *__restrict__ acc, const float *__restrict__ gr
             }
             bad = bad || !isfinite(g);
             if (MODE == 1) {
-                grad_out[(size_t)k * P + v] = g;
+                grad_out[(size_t)(k - k0r) * P + v] = g;
             } else {
                 const float b1 = 0.9f, b2 = 0.999f, eps = 1e-8f;
                 const float lri = v < 2 ? lr.mu : (v < 5 ? lr.chol : (v == 5 ? lr.log_pi : (((v - 6) % E) == 0 ? lr.expert : lr.slope)));
@@ -1517,15 +1572,17 @@ k_adam(int K, ParamsMut p, float *__restrict__ acc, const float *__restrict__ gr
 // needed; measured faster at K >= 20 000).
 template <int C, int E, int MODE>
 __global__ void __launch_bounds__(64)
-k_adam_kt(int K, ParamsMut p, float *__restrict__ acc, const float *__restrict__ grad_in,
+k_adam_kt(AdamCommon cm, ParamsMut p, float *__restrict__ acc, const float *__restrict__ grad_in,
        float *__restrict__ grad_out, float *__restrict__ m1, float *__restrict__ m2,
        LrDev lr, HandleCtr *hc, const GridCtr *gc, long long cap)
 {
     using R = Rec<C, E>;
     constexpr int P = R::P;
-    if (MODE != 2 && gc->skip) return;
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    const bool live = k < K;
+    if (adam_skipped<P, MODE>(cm, grad_out, gc)) return;
+    const int K = cm.Ktot;
+    const int kr = blockIdx.x * blockDim.x + threadIdx.x;   // row of grad_in / grad_out
+    const int k = cm.k0 + kr;
+    const bool live = kr < cm.n;
     const long long t = hc->t + 1;
     if (live) {
         // every load first (they are independent and overlap), then compute,
@@ -1542,7 +1599,7 @@ k_adam_kt(int K, ParamsMut p, float *__restrict__ acc, const float *__restrict__
         float raw[R::V];
         if (MODE == 2) {
 #pragma unroll
-            for (int i = 0; i < P; i++) g[i] = grad_in[(size_t)k * P + i];
+            for (int i = 0; i < P; i++) g[i] = grad_in[(size_t)kr * P + i];
         } else {
             const float4 *ap = reinterpret_cast<const float4 *>(acc) + (size_t)k * (R::V / 4);
 #pragma unroll
@@ -1585,7 +1642,7 @@ k_adam_kt(int K, ParamsMut p, float *__restrict__ acc, const float *__restrict__
         if (!ok) atomicExch((unsigned long long *)&hc->nonfinite, 1ull);
         if (MODE == 1) {
 #pragma unroll
-            for (int i = 0; i < P; i++) grad_out[(size_t)k * P + i] = g[i];
+            for (int i = 0; i < P; i++) grad_out[(size_t)kr * P + i] = g[i];
         } else {
             const float b1 = 0.9f, b2 = 0.999f, eps = 1e-8f;
             // 1 - beta^t = -expm1(t log(beta)), accurate to a few ulp for every t

@@ -148,7 +148,7 @@ smoe_status smoe_segment_init(const float *image, int H, int W, int C, const int
                               float *log_pi, float *expert)
 {
     if (!image || !labels || !mu || !chol || !log_pi || !expert || n_segments < 1 || K < 1 ||
-        !(expert_order == 0 || expert_order == 1) || !(scale_px > 0.f))
+        !(expert_order == 0 || expert_order == 1) || !(scale_px > 0.f) || H < 1 || W < 1 || C < 1)
         return SMOE_ERR_INVALID_ARG;
     if (K < n_segments) return SMOE_ERR_INVALID_ARG;   // SPEC TooFewKernels
     const size_t npx = (size_t)H * W;
@@ -158,6 +158,10 @@ smoe_status smoe_segment_init(const float *image, int H, int W, int C, const int
         if (l < 0 || l >= n_segments) return SMOE_ERR_INVALID_ARG;
         members[l].push_back(i);
     }
+    // every segment id must own a pixel (its kernels are placed on its pixels
+    // and its expert is its mean colour)
+    for (int s = 0; s < n_segments; s++)
+        if (members[s].empty()) return SMOE_ERR_INVALID_ARG;
     // budget: max(1, floor(K |R|/N)) then largest remainder to exactly K
     std::vector<long long> cnt(n_segments);
     std::vector<double> rem(n_segments);

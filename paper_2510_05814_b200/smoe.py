@@ -50,10 +50,11 @@ class c_kernel_time(ctypes.Structure):
 
 
 class c_work(ctypes.Structure):
-    _fields_ = [("tested_pairs", ctypes.c_longlong), ("hit_pairs", ctypes.c_longlong)]
+    _fields_ = [("tested_pairs", ctypes.c_longlong), ("hit_pairs", ctypes.c_longlong),
+                ("sort_cycles", ctypes.c_longlong), ("cta_cycles", ctypes.c_longlong)]
 
 
-KERNEL_COUNT = 5
+KERNEL_COUNT = 7
 
 
 class c_raw_stats(ctypes.Structure):
@@ -97,6 +98,7 @@ def lib():
         "smoe_set_band": (st, [H, I, I]),
         "smoe_grad": (st, [H, ctypes.POINTER(c_params), P, P, P]),
         "smoe_apply": (st, [H, ctypes.POINTER(c_params), P, ctypes.POINTER(c_lr)]),
+        "smoe_apply_ex": (st, [H, ctypes.POINTER(c_params), P, ctypes.POINTER(c_lr), I, I, P]),
         "smoe_reset_adam": (st, [H]),
         "smoe_sync": (st, [H, ctypes.POINTER(c_stats)]),
         "smoe_bin": (st, [H, ctypes.POINTER(c_params), I, I, P, P, ctypes.c_longlong,
@@ -151,10 +153,19 @@ class Params:
         K = self.mu.shape[0]
         return torch.cat([self.mu, self.chol, self.log_pi[:, None], self.expert.reshape(K, -1)], 1)
 
-    def c(self) -> c_params:
+    def c(self, K: int | None = None, C: int | None = None, E: int | None = None,
+          device: int | None = None) -> c_params:
         for t in (self.mu, self.chol, self.log_pi, self.expert):
             if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
                 raise SmoeError(ERR_INVALID_ARG, "params must be contiguous float32 CUDA tensors")
+            if device is not None and t.device.index != device:
+                raise SmoeError(ERR_INVALID_ARG, f"params on {t.device}, the handle is on cuda:{device}")
+        if K is not None:
+            want = {"mu": 2 * K, "chol": 3 * K, "log_pi": K, "expert": K * C * E}
+            for name, n in want.items():
+                if getattr(self, name).numel() < n:
+                    raise SmoeError(ERR_INVALID_ARG, f"params.{name}: {getattr(self, name).numel()} "
+                                                     f"elements, expected {n}")
         return c_params(self.mu.data_ptr(), self.chol.data_ptr(), self.log_pi.data_ptr(),
                         self.expert.data_ptr())
 
@@ -192,19 +203,35 @@ class Stats:
         return Stats(s.loss, s.psnr_db, s.sse, s.sse_clamped, s.pairs, s.uncovered_px, s.n_tiles)
 
 
-def _ptr(x):
-    """Raw address of a contiguous torch tensor or numpy array (host or device)."""
+def _ptr(x, what="buffer", dtype=torch.float32, numel=None, device=None):
+    """Raw address of a contiguous torch tensor or numpy array (host or
+    device) after checking what the library will read through it: dtype,
+    element count (at least ``numel``) and, for CUDA tensors, the handle's
+    device.  A mismatch raises ERR_INVALID_ARG instead of letting the library
+    read the wrong bytes or copy past the end of a host buffer."""
     if x is None:
         return None
     if isinstance(x, torch.Tensor):
         if not x.is_contiguous():
-            raise SmoeError(ERR_INVALID_ARG, "buffers must be contiguous")
+            raise SmoeError(ERR_INVALID_ARG, f"{what}: must be contiguous")
+        if x.dtype != dtype:
+            raise SmoeError(ERR_INVALID_ARG, f"{what}: dtype {x.dtype}, expected {dtype}")
+        if numel is not None and x.numel() < numel:
+            raise SmoeError(ERR_INVALID_ARG, f"{what}: {x.numel()} elements, expected {numel}")
+        if x.is_cuda and device is not None and x.device.index != device:
+            raise SmoeError(ERR_INVALID_ARG, f"{what}: on {x.device}, the handle is on cuda:{device}")
         return x.data_ptr()
     if hasattr(x, "ctypes") and hasattr(x, "flags"):
+        import numpy as np
         if not x.flags["C_CONTIGUOUS"]:
-            raise SmoeError(ERR_INVALID_ARG, "buffers must be contiguous")
+            raise SmoeError(ERR_INVALID_ARG, f"{what}: must be contiguous")
+        want = np.float32 if dtype == torch.float32 else np.float64
+        if x.dtype != want:
+            raise SmoeError(ERR_INVALID_ARG, f"{what}: dtype {x.dtype}, expected {np.dtype(want)}")
+        if numel is not None and x.size < numel:
+            raise SmoeError(ERR_INVALID_ARG, f"{what}: {x.size} elements, expected {numel}")
         return x.ctypes.data
-    return x
+    raise SmoeError(ERR_INVALID_ARG, f"{what}: expected a torch tensor or numpy array")
 
 
 class SMoE:
@@ -248,18 +275,24 @@ class SMoE:
         s = torch.cuda.current_stream(self.device).cuda_stream
         _check(lib().smoe_set_stream(self.h, ctypes.c_void_p(s)), self.h)
 
+    def _p(self, params: Params) -> c_params:
+        return params.c(self.K, self.C, self.E, self.device)
+
+    def _target(self, target):
+        return _ptr(target, "target", torch.float32, self.C * self.H * self.W, self.device)
+
     def step(self, params: Params, target, lr: LR | None = None, stats: bool = True):
         """smoe_step: one fit iteration in place on ``params``; returns the
         pre-update Stats when ``stats`` (synchronising), else None."""
         self._stream()
         lr = lr or LR()
-        p = params.c()
+        p = self._p(params)
+        t = self._target(target)
         if stats:
             s = c_stats()
-            _check(lib().smoe_step(self.h, ctypes.byref(p), _ptr(target), ctypes.byref(lr.c()),
-                                   ctypes.byref(s)), self.h)
+            _check(lib().smoe_step(self.h, ctypes.byref(p), t, ctypes.byref(lr.c()), ctypes.byref(s)), self.h)
             return Stats.of(s)
-        _check(lib().smoe_step(self.h, ctypes.byref(p), _ptr(target), ctypes.byref(lr.c()), None), self.h)
+        _check(lib().smoe_step(self.h, ctypes.byref(p), t, ctypes.byref(lr.c()), None), self.h)
         return None
 
     def render(self, params: Params, out_H: int | None = None, out_W: int | None = None, out=None,
@@ -270,11 +303,24 @@ class SMoE:
         self._stream()
         out_H = self.H if out_H is None else out_H
         out_W = self.W if out_W is None else out_W
-        if out is None:
+        own = out is None
+        if own:
             out = torch.empty((self.C, out_H, out_W), dtype=torch.float32, device=f"cuda:{self.device}")
         ro = c_render_options(sharpen, accumulate)
-        _check(lib().smoe_render_ex(self.h, ctypes.byref(params.c()), out_H, out_W, _ptr(out), ctypes.byref(ro)),
-               self.h)
+        args = (self.h, ctypes.byref(self._p(params)), out_H, out_W,
+                _ptr(out, "out", torch.float32, self.C * out_H * out_W, self.device), ctypes.byref(ro))
+        _check(lib().smoe_render_ex(*args), self.h)
+        if own:
+            # the output is ours: make sure the render was not skipped by a
+            # list overflow (the library grows its lists and we render again)
+            for attempt in range(3):
+                try:
+                    self.sync()
+                    break
+                except SmoeError as e:
+                    if e.status != ERR_CAPACITY or attempt == 2:
+                        raise
+                    _check(lib().smoe_render_ex(*args), self.h)
         return out
 
     def set_band(self, tile_row0: int, tile_row1: int):
@@ -287,14 +333,23 @@ class SMoE:
         if grad is None:
             grad = torch.empty((self.K, self.Pk), dtype=torch.float32, device=dev)
         if sums is None:
-            sums = torch.empty(3, dtype=torch.float64, device=dev)
-        _check(lib().smoe_grad(self.h, ctypes.byref(params.c()), _ptr(target), _ptr(grad), _ptr(sums)), self.h)
+            sums = torch.empty(4, dtype=torch.float64, device=dev)
+        _check(lib().smoe_grad(self.h, ctypes.byref(self._p(params)), self._target(target),
+                               _ptr(grad, "grad", torch.float32, self.K * self.Pk, self.device),
+                               _ptr(sums, "sums", torch.float64, 4, self.device)), self.h)
         return grad, sums
 
-    def apply(self, params: Params, grad, lr: LR | None = None):
+    def apply(self, params: Params, grad, lr: LR | None = None, k0: int = 0, k1: int | None = None,
+              sums=None):
+        """smoe_apply / smoe_apply_ex: Adam update of kernels [k0, k1) with
+        grad[(k1-k0), Pk]; ``sums`` (the all-reduced smoe_grad sums[4]) makes
+        the update conditional on no rank having skipped its band."""
         self._stream()
-        _check(lib().smoe_apply(self.h, ctypes.byref(params.c()), _ptr(grad), ctypes.byref((lr or LR()).c())),
-               self.h)
+        k1 = self.K if k1 is None else k1
+        _check(lib().smoe_apply_ex(self.h, ctypes.byref(self._p(params)),
+                                   _ptr(grad, "grad", torch.float32, (k1 - k0) * self.Pk, self.device),
+                                   ctypes.byref((lr or LR()).c()), int(k0), int(k1),
+                                   _ptr(sums, "sums", torch.float64, 4, self.device)), self.h)
 
     def reset_adam(self):
         _check(lib().smoe_reset_adam(self.h), self.h)
@@ -311,7 +366,9 @@ class SMoE:
         """smoe_set_adam: restore an optimiser checkpoint."""
         m1 = m1.contiguous().float()
         m2 = m2.contiguous().float()
-        _check(lib().smoe_set_adam(self.h, _ptr(m1), _ptr(m2), int(t)), self.h)
+        n = self.K * self.Pk
+        _check(lib().smoe_set_adam(self.h, _ptr(m1, "m1", numel=n, device=self.device),
+                                   _ptr(m2, "m2", numel=n, device=self.device), int(t)), self.h)
 
     def stats_async(self, dst_ptr: int):
         """smoe_stats_async: enqueue the D2H copy of the last step's raw
@@ -338,10 +395,10 @@ class SMoE:
         rng = torch.empty(nt + 1, dtype=torch.int32)
         tb = torch.empty((self.K, 4), dtype=torch.int32)
         n = ctypes.c_longlong()
-        _check(lib().smoe_bin(self.h, ctypes.byref(params.c()), out_H, out_W, rng.data_ptr(), None, 0,
+        _check(lib().smoe_bin(self.h, ctypes.byref(self._p(params)), out_H, out_W, rng.data_ptr(), None, 0,
                               ctypes.byref(n), tb.data_ptr()), self.h)
         ids = torch.empty(max(1, n.value), dtype=torch.int32)
-        _check(lib().smoe_bin(self.h, ctypes.byref(params.c()), out_H, out_W, rng.data_ptr(), ids.data_ptr(),
+        _check(lib().smoe_bin(self.h, ctypes.byref(self._p(params)), out_H, out_W, rng.data_ptr(), ids.data_ptr(),
                               ids.numel(), ctypes.byref(n), tb.data_ptr()), self.h)
         return rng.long(), ids[:n.value].long(), tb.long()
 
@@ -364,7 +421,9 @@ class SMoE:
         _check(lib().smoe_profile_begin(self.h, int(max_launches), mask), self.h)
 
     def profile_end(self):
-        """smoe_profile_end -> ({kernel name: (total_ms, launches)}, (tested, hit))."""
+        """smoe_profile_end -> ({kernel name: (total_ms, launches)}, (tested, hit)).
+        ``self.last_work`` keeps the full counters (tested, hit, sort cycles,
+        CTA cycles)."""
         arr = (c_kernel_time * KERNEL_COUNT)()
         w = c_work()
         _check(lib().smoe_profile_end(self.h, ctypes.cast(arr, ctypes.c_void_p), ctypes.byref(w)), self.h)
@@ -372,6 +431,7 @@ class SMoE:
         for i in range(KERNEL_COUNT):
             if arr[i].launches:
                 out[lib().smoe_kernel_name(i).decode()] = (arr[i].total_ms, arr[i].launches)
+        self.last_work = (w.tested_pairs, w.hit_pairs, w.sort_cycles, w.cta_cycles)
         return out, (w.tested_pairs, w.hit_pairs)
 
 

@@ -57,3 +57,47 @@ def assert_grads(g, g_ref, a_ref, rel=1e-4, floor=1e-5, what="grad"):
         i = np.unravel_index(np.argmax(d / np.maximum(tol, 1e-300)), d.shape)
         raise AssertionError(f"{what}: {bad.sum()} of {bad.size} out of tolerance; worst at {i}: "
                              f"gpu {g[i]:.6e} ref {g_ref[i]:.6e} A {a_ref[i]:.3e}")
+
+
+def oracle_fit_with_tolerance(op, target, T, lr_of_t, R2=None, rel=1e-4, floor=1e-5):
+    """Oracle fit (dense loss + analytic gradient + Adam per step) that
+    also returns, per parameter component, how far an fp32 run may drift from
+    it after T steps when its gradient meets the north-star tolerance
+    tol_g = rel|g| + floor A_ref at every step ("Trajectory
+    tolerance").  Adam divides the first moment by sqrt(v), so a gradient
+    error tol_g moves a step by at most lr * 2 tol_g / sqrt(v) (first-order
+    in m and v), and never by more than 2 lr max(1, |m^|/sqrt(v^)) (two
+    updates of opposite sign: a component whose gradient is below tol_g has
+    an undetermined sign).  fp32 storage adds half an ulp of the parameter
+    per step.  Returns (params, trace[(loss, psnr)], tol[K][Pk])."""
+    opt = O.Adam(op.K, op.Pk)
+    p = op.copy()
+    tol = np.zeros((op.K, op.Pk))
+    trace = []
+    for t in range(T):
+        lg = O.loss_grad(p, target, R2=R2)
+        trace.append((lg.loss, lg.psnr))
+        lr = lr_of_t(t)
+        lrv = lr.vector(op.C, op.order)[None, :]
+        p = opt.step(p, lg.grad, lr)
+        mhat = opt.m1 / (1.0 - O.BETA1 ** opt.t)
+        rms = np.sqrt(opt.m2 / (1.0 - O.BETA2 ** opt.t)) + O.EPS
+        tg = rel * np.abs(lg.grad) + floor * lg.grad_abs
+        cap = 2.0 * np.maximum(1.0, np.abs(mhat) / rms)
+        tol += lrv * np.minimum(cap, 2.0 * tg / rms) + 2.0 ** -24 * np.abs(p.flat())
+    return p, trace, tol
+
+
+def assert_params(got, ref, tol, factor=2.0, what="params"):
+    """Every component within factor x tol (no outlier budget); the factor
+    covers the feedback of parameter differences into later gradients, which
+    the first-order tol of oracle_fit_with_tolerance leaves out."""
+    got = np.asarray(got, np.float64)
+    d = np.abs(got - ref)
+    lim = factor * tol
+    bad = d > lim
+    if bad.any():
+        i = np.unravel_index(np.argmax(d / np.maximum(lim, 1e-300)), d.shape)
+        raise AssertionError(f"{what}: {bad.sum()} of {bad.size} beyond {factor} x tol; worst at {i}: "
+                             f"gpu {got[i]:.8e} ref {ref[i]:.8e} tol {tol[i]:.3e}")
+    return float((d / np.maximum(lim, 1e-300)).max())

@@ -37,5 +37,5 @@ def test_bench_two_ranks_json_line(config):
     assert d["value"] > 0 and d["ms_per_step"] > 0
     assert d["gpu_launches"] > 0
     e = d["e2e"]
-    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] == 48
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] == 64
     assert d["fit_stats"]["loss"] == d["fit_stats"]["loss"]   # finite

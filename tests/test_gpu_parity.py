@@ -13,7 +13,8 @@ import torch
 
 import oracle as O
 from paper_2510_05814_b200 import smoe, synth
-from helpers import assert_grads, assert_pixels, conditioned, conditioned_multi
+from helpers import (assert_grads, assert_params, assert_pixels, conditioned, conditioned_multi,
+                     oracle_fit_with_tolerance)
 
 pytestmark = pytest.mark.gpu
 
@@ -53,15 +54,35 @@ def test_binning_bit_exact(H, W, C, K, order, scale, seed):
     np.testing.assert_array_equal(ids.numpy(), ids_ref)
 
 
-@pytest.mark.parametrize("fused", ["0", "1"])
-def test_binning_both_binners(fused, monkeypatch):
-    """The cooperative fused binner (k_bin) and the three-kernel one produce
-    the same canonical lists, with and without a band."""
-    monkeypatch.setenv("SMOE_FUSED_BIN", fused)
+# The three binners of a1-a3 and the kernels each launches
+# (profiled by name through the C ABI, so a test cannot silently run
+# another path): direct buckets (default, <= 2^18 blocks); CSR lists with the
+# single-CTA scan and LPT block order in k_preprocess's last CTA + k_scatter;
+# CSR lists from the cooperative fused binner k_bin.
+BINNERS = {
+    "direct": ({}, {"k_preprocess", "k_raster<render>"}),
+    "csr_scan_lpt": ({"SMOE_CSR": "1", "SMOE_FUSED_BIN": "0"}, {"k_preprocess", "k_scatter", "k_raster<render>"}),
+    "csr_coop": ({"SMOE_CSR": "1", "SMOE_FUSED_BIN": "1"}, {"k_bin", "k_raster<render>"}),
+}
+
+
+@pytest.mark.parametrize("binner", list(BINNERS))
+def test_binning_all_binners(binner, monkeypatch):
+    """Every binner produces the canonical lists (bit-exact), launches the
+    kernels it is meant to, and feeds a raster whose per-band gradients sum
+    to the oracle's full-image gradient."""
+    env, kernels = BINNERS[binner]
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
     H, W, C, K = 130, 97, 3, 600
     pool = conditioned(synth.aniso_pool(H, W, C, K, 5, order=1, margin_px=8), H, W)
     h = smoe.SMoE(K, H, W, C, 1)
-    rng, ids, tb = h.bin(dev_pool(pool))
+    p = dev_pool(pool)
+    h.bin(p)                                      # first binning calibrates the capacity
+    h.profile_begin(64)
+    rng, ids, tb = h.bin(p)
+    launched, _ = h.profile_end()
+    assert set(launched) == kernels, launched
     _, tb_ref, _ = O.boxes(opar(pool), H, W)
     rng_ref, ids_ref = O.tile_list(tb_ref, 7, 9)
     np.testing.assert_array_equal(rng.numpy(), rng_ref)
@@ -71,8 +92,9 @@ def test_binning_both_binners(fused, monkeypatch):
     acc = None
     for r0, r1 in [(0, 4), (4, 9)]:
         h.set_band(r0, r1)
-        g, _ = h.grad(dev_pool(pool), target)
-        acc = g if acc is None else acc + g
+        for _ in range(2):                        # eager (calibrating) pass, then graph replay
+            g, _ = h.grad(p, target)
+        acc = g.clone() if acc is None else acc + g
     assert_grads(acc.cpu().numpy(), lg.grad, lg.grad_abs)
 
 
@@ -109,6 +131,27 @@ def test_binning_large_bucket_merge_path():
     assert (rng_ref[1:] - rng_ref[:-1]).max() > 2048
     np.testing.assert_array_equal(rng.numpy(), rng_ref)
     np.testing.assert_array_equal(ids.numpy(), ids_ref)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_grad_parity_bucket_over_2048(mode):
+    """Gradients of a block whose list (5000 kernels) exceeds the in-smem
+    sort (2048: CTA merge sort through global scratch) and spans 40 record
+    batches of 128 (the kernel-parallel backward rebuilds its ballot records
+    per batch)."""
+    H, W, K = 32, 32, 5000
+    g = np.random.default_rng(0)
+    pool = synth.aniso_pool(H, W, 1, K, 9, l_range=(0.3, 0.6), shear=0.1, log_pi_sd=0.3)
+    pool.mu[:] = g.uniform(18.2, 29.8, (K, 2)).astype(np.float32)
+    pool = conditioned(pool, H, W)
+    target = synth.image(H, W, 1, 10)
+    h = smoe.SMoE(K, H, W, 1, 0, backward_mode=mode)
+    rng, _, _ = h.bin(dev_pool(pool))
+    assert int((rng[1:] - rng[:-1]).max()) > 2048
+    gr, sums = h.grad(dev_pool(pool), torch.as_tensor(target).cuda())
+    lg = O.loss_grad(opar(pool), target.astype(np.float64))
+    assert abs(float(sums[0]) - lg.sse) <= 1e-5 * lg.sse
+    assert_grads(gr.cpu().numpy(), lg.grad, lg.grad_abs)
 
 
 @pytest.mark.parametrize("direct_max", ["", "32768"])
@@ -241,8 +284,9 @@ def test_grad_host_buffers_and_uncovered():
     target = synth.image(H, W, C, 6)
     h = smoe.SMoE(K, H, W, C, 1)
     g = np.zeros((K, h.Pk), np.float32)
-    sums = np.zeros(3)
+    sums = np.zeros(4)
     h.grad(dev_pool(pool), target, grad=g, sums=sums)   # host target, grad, sums
+    assert sums[3] == 0.0
     lg = O.loss_grad(opar(pool), target.astype(np.float64))
     assert lg.uncovered > 0 and int(sums[2]) == lg.uncovered
     assert_grads(g, lg.grad, lg.grad_abs)
@@ -350,8 +394,10 @@ def test_capacity_overflow_is_recovered():
 @pytest.mark.parametrize("init", ["paper", "aniso"])
 def test_fit_100_iterations(init):
     """Config 1 geometry (64x64 gray, 64 kernels, constant experts): PSNR
-    after 100 Adam iterations within 0.01 dB of the oracle, parameters within
-    1e-3 relative (floor: lr x iterations x 1e-3)."""
+    after 100 Adam iterations within 0.01 dB of the oracle, and EVERY
+    parameter within the trajectory tolerance (helpers.oracle_fit_with_
+    tolerance: the north-star gradient tolerance propagated through Adam's
+    normalisation) -- no outlier budget."""
     H, W, C, K, T = 64, 64, 1, 64, 100
     target = synth.image(H, W, C, 1235)
     if init == "paper":
@@ -366,17 +412,15 @@ def test_fit_100_iterations(init):
     for t in range(T):
         st = h.step(p, tg, smoe.LR.paper(t, T))
         trace.append(st.psnr_db)
-    q, otrace = O.fit(opar(pool), target.astype(np.float64), T)
+    q, otrace, tol = oracle_fit_with_tolerance(opar(pool), target.astype(np.float64), T,
+                                               lambda t: O.LR(O.lr_mu_schedule(t, T)))
     final = O.loss_grad(q, target.astype(np.float64)).psnr
     fin_gpu = h.grad(p, tg)[1][1].item()
     psnr_gpu = 10 * np.log10(H * W * C / fin_gpu)
     assert abs(psnr_gpu - final) < 0.01, (psnr_gpu, final)
-    assert abs(trace[-1] - otrace[-1][1]) < 0.01
-    got = p.flat().cpu().numpy().astype(np.float64)
-    ref = q.flat()
-    lrv = O.LR().vector(C, 0)
-    tol = 1e-3 * np.abs(ref - opar(pool).flat()) + 1e-3 * lrv[None, :] * 10
-    assert (np.abs(got - ref) <= tol + 1e-5 * np.abs(ref)).mean() > 0.99
+    assert max(abs(a - b[1]) for a, b in zip(trace, otrace)) < 0.01
+    worst = assert_params(p.flat().cpu().numpy(), q.flat(), tol)
+    print(f"worst |dp| / (2 tol) = {worst:.3f}")
 
 
 # --------------------------------------------------- full-size sampled ------
@@ -590,37 +634,57 @@ def test_host_target_pipelined_steps_match_device_target():
 
 # ------------------------------------------- full-size configs, sampled ----
 
-def _sampled_parity(cfg, n_px=1500, n_kern=4, sr=None, seed=0):
+def _sampled_parity(cfg, n_px=1500, n_kern=8, sr=None, seed=0):
+    """A BASELINE.json config at full size, in the launch configuration
+    bench.py times (same handle options, graph replay), against the dense
+    oracle on samples: n_px output pixels (each dense over all K kernels)
+    and n_kern kernels' full-image gradients.  The workload's pool is first
+    margin-conditioned (rule P1, over every (pixel, kernel) pair of the
+    raster: O.margins covers each kernel's padded box) with the wider
+    margins SURVEY §8(c) requires at >= 4096-px coordinates, so fp32 and
+    fp64 take the same cull and box decisions and the north-star
+    tolerances apply to every sample with no failure allowed.  An SR raster
+    has 16x the samples per kernel, too many to clear every pair by
+    jittering; there the sampled output pixels are the ones whose dense
+    margin min_j |d_j^2 - R2| exceeds 1e-2 (O.point_margins; that also keeps
+    them >= r 1e-2 / (2 R2) px inside every listing box, far above the fp32
+    rounding of 8160-px coordinates)."""
     target, _, pool = synth.workload(cfg)
     C, H, W = target.shape
     order = (pool.expert.shape[2] - 1) // 2
+    oH, oW = (H * sr, W * sr) if sr else (H, W)
+    pool = conditioned(pool, H, W, seed=seed)
     g = np.random.default_rng(seed)
     h = smoe.SMoE(pool.K, H, W, C, order)
     p = dev_pool(pool)
     op = opar(pool)
-    # unconditioned paper-init pools: compare only samples away from the
-    # discontinuities (oracle margin check on the sampled kernels' pixels)
-    oH, oW = (H * sr, W * sr) if sr else (H, W)
     y = h.render(p, oH, oW).cpu().numpy()
-    ix, iy = g.integers(0, oW, n_px), g.integers(0, oH, n_px)
-    xs, ys = (ix + 0.5) * W / oW - 0.5, (iy + 0.5) * H / oH - 0.5
-    y_ref, _ = O.render_points(op, xs, ys)
-    d = np.abs(y[:, iy, ix].T - y_ref)
-    tol = 1e-5 * np.abs(y_ref) + 1e-6
-    # a sample within fp32 rounding of a kernel's cull boundary may flip
-    # (rule P1 is not applied to the full-size workload): allow <= 0.2%
-    assert (d > tol).mean() <= 2e-3, (d > tol).mean()
+    if sr:
+        ix, iy = g.integers(0, oW, 3 * n_px), g.integers(0, oH, 3 * n_px)
+        xs, ys = (ix + 0.5) * W / oW - 0.5, (iy + 0.5) * H / oH - 0.5
+        keep = np.flatnonzero(O.point_margins(op, xs, ys) > 1e-2)[:n_px]
+        assert keep.size == n_px
+        ix, iy, xs, ys = ix[keep], iy[keep], xs[keep], ys[keep]
+    else:
+        ix, iy = g.integers(0, oW, n_px), g.integers(0, oH, n_px)
+        xs, ys = ix.astype(np.float64), iy.astype(np.float64)
+    y_ref, D_ref = O.render_points(op, xs, ys)
+    assert (D_ref > 0).mean() > 0.9
+    assert_pixels(y[:, iy, ix].T, y_ref, what=f"{cfg} x{sr or 1} sampled pixels")
     if sr:
         return
-    grad, sums = h.grad(p, torch.as_tensor(target).cuda())
-    st = O.loss_grad  # noqa
-    sel = g.choice(pool.K, n_kern, replace=False)
-    dg, da = O.margins(O.Params(op.mu[sel], op.chol[sel], op.log_pi[sel], op.expert[sel]), H, W)
-    sel = sel[(dg > 1e-3) & (da > 1e-3)]
+    tg = torch.as_tensor(target).cuda()
+    for _ in range(2):                      # eager calibrating pass, then the graph bench.py replays
+        grad, sums = h.grad(p, tg)
+    assert float(sums[3]) == 0.0
+    # kernels whose box lies inside the image (their gradient sums a full
+    # ellipse of pixels)
+    _, tb, _ = O.boxes(op, H, W)
+    inside = np.flatnonzero((tb[:, 0] > 0) & (tb[:, 2] > 0) & (tb[:, 1] < (W - 1) // 16) &
+                            (tb[:, 3] < (H - 1) // 16))
+    sel = np.sort(g.choice(inside, n_kern, replace=False))
     g_ref, a_ref = O.grad_kernels(op, target.astype(np.float64), sel)
-    gg = grad.cpu().numpy()[sel]
-    # neighbours of a sampled kernel may sit on a boundary: relative floor 1e-4 A
-    assert_grads(gg, g_ref, a_ref, floor=1e-4)
+    assert_grads(grad.cpu().numpy()[sel], g_ref, a_ref, what=f"{cfg} sampled kernels")
 
 
 def test_config3_div2k_full_size_sampled():
@@ -632,14 +696,14 @@ def test_config3_div2k_4x_render_sampled():
 
 
 def test_config4_denoise_full_size_sampled():
-    _sampled_parity("denoise", n_kern=6)
+    _sampled_parity("denoise")
 
 
 def test_config5_8k_full_size_sampled():
     """Config 5 (7680x4320x3, 1M kernels; the multi-GPU workload) on one GPU:
-    sampled pixels and one sampled kernel's gradient against the dense oracle
+    sampled pixels and 8 sampled kernels' gradients against the dense oracle
     (every sample is evaluated over all 10^6 kernels)."""
-    _sampled_parity("8k", n_px=400, n_kern=2, seed=1)
+    _sampled_parity("8k", n_px=400, n_kern=8, seed=1)
 
 
 def test_checkpoint_resume():

@@ -544,3 +544,74 @@ def test_sharpening_spec_examples():
     q.expert[:] = 0.625
     yq, Dq = O.render(q, H, W, 60, 68)
     assert np.all(np.abs(yq[0][Dq > 0] - 0.625) < 1e-15)
+
+
+def test_sr_sampling_downsample_consistency_linear():
+    """SR sample mapping of oracle_render (S:547 half-pixel convention; P:162,
+    P:314).  A single untruncated (R2 = inf) linear-expert kernel renders the
+    plane y = m + W (x - mu) exactly at every sample.  Averaging each k x k
+    block of the k-times render must give the 1x render exactly: the mean of
+    the k output sample positions (j+1/2)/k - 1/2 of source pixel i is i.
+    S:565's low-frequency consistency check, exact for a linear model.  A
+    mapping x = j/k (offset -(k-1)/(2k)) or the corner-aligned
+    j (W-1)/(kW-1) fails it by far more than rounding."""
+    H, W = 7, 9
+    p = params([[3.3, 2.6]], [[4.0, 0.7, 3.0]], [[0.4]], order=1)
+    p.expert[0, 0, 1:] = [0.031, -0.017]         # Wx, Wy
+    y1, _ = O.render(p, H, W, R2=INF)
+    for k in (2, 3, 4):
+        yk, Dk = O.render(p, H, W, k * H, k * W, R2=INF)
+        assert (Dk > 0).all()
+        down = yk.reshape(1, H, k, W, k).mean(axis=(2, 4))
+        np.testing.assert_allclose(down, y1, rtol=0, atol=1e-13)
+    # the same plane at a non-integer scale: every sample is the plane at
+    # its mapped point, so the output is itself a plane whose values at the
+    # two outermost samples are symmetric about the image centre
+    y15, _ = O.render(p, H, W, 11, 14, R2=INF)
+    row = y15[0, 5]
+    np.testing.assert_allclose(row[0] + row[-1], 2 * row.mean(), atol=1e-13)
+
+
+def test_sr_sampling_mirror_symmetry():
+    """A model mirror-symmetric about the image's vertical centre line
+    x = (W-1)/2 must render mirror-symmetric at any output size, integer or
+    not, when samples are centred.  Checks the mapping itself with a
+    nonlinear, truncated, anisotropic model (not only planes)."""
+    H, W = 20, 26
+    g = np.random.default_rng(5)
+    K = 12
+    mu = np.stack([g.uniform(2, 11, K), g.uniform(2, 18, K)], 1)
+    ch = np.stack([g.uniform(1.5, 3.5, K), g.uniform(-1.0, 1.0, K), g.uniform(1.5, 3.5, K)], 1)
+    m = g.uniform(0.1, 0.9, (K, 2))
+    mir_mu = np.stack([(W - 1) - mu[:, 0], mu[:, 1]], 1)
+    mir_ch = ch * np.array([1.0, -1.0, 1.0])     # Sigma_xy -> -Sigma_xy under x -> -x
+    p = params(np.concatenate([mu, mir_mu]), np.concatenate([ch, mir_ch]), np.concatenate([m, m]))
+    for oH, oW in [(20, 26), (40, 52), (31, 37), (50, 61)]:
+        y, _ = O.render(p, H, W, oH, oW)
+        np.testing.assert_allclose(y, y[:, :, ::-1], rtol=0, atol=1e-12)
+
+
+def test_point_margins_against_numpy():
+    """O.point_margins (sampled-parity conditioning) equals the minimum over
+    kernels of |delta^T Sigma^-1 delta - R2| computed with numpy's inverse of
+    Sigma = L L^T; a point on a kernel's ellipse has margin 0 and a kernel
+    centre alone gives R2."""
+    g = np.random.default_rng(11)
+    K = 25
+    mu = g.uniform(0, 30, (K, 2))
+    ch = np.stack([g.uniform(1, 4, K), g.uniform(-2, 2, K), g.uniform(1, 4, K)], 1)
+    p = params(mu, ch, g.uniform(0, 1, K))
+    xs, ys = g.uniform(-3, 33, 200), g.uniform(-3, 33, 200)
+    R2 = O.R2_99()
+    ref = np.full(200, np.inf)
+    for k in range(K):
+        L = np.array([[ch[k, 0], 0], [ch[k, 1], ch[k, 2]]])
+        Si = np.linalg.inv(L @ L.T)
+        d = np.stack([xs - mu[k, 0], ys - mu[k, 1]], 1)
+        ref = np.minimum(ref, np.abs(np.einsum("ni,ij,nj->n", d, Si, d) - R2))
+    np.testing.assert_allclose(O.point_margins(p, xs, ys), ref, rtol=1e-12, atol=1e-12)
+    one = params([[5.0, 7.0]], [[2.0, 0.5, 1.5]], [0.3])
+    L = np.array([[2.0, 0.0], [0.5, 1.5]])
+    v = L @ np.array([np.cos(0.7), np.sin(0.7)]) * np.sqrt(R2)     # on the ellipse
+    assert O.point_margins(one, [5.0 + v[0]], [7.0 + v[1]])[0] < 1e-12
+    assert abs(O.point_margins(one, [5.0], [7.0])[0] - R2) < 1e-12
