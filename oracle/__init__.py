@@ -65,9 +65,9 @@ def _lib():
         lib.oracle_render_points.restype = None
         lib.oracle_render_points.argtypes = [I, I, I, P, P, P, P, I, P, P, D, P, P]
         lib.oracle_loss_grad.restype = None
-        lib.oracle_loss_grad.argtypes = [I, I, I, P, P, P, P, I, I, P, I, I, D, P, P, P]
+        lib.oracle_loss_grad.argtypes = [I, I, I, P, P, P, P, I, I, P, I, I, D, P, P, P, P]
         lib.oracle_grad_kernels.restype = None
-        lib.oracle_grad_kernels.argtypes = [I, I, I, P, P, P, P, I, I, P, D, I, P, P, P]
+        lib.oracle_grad_kernels.argtypes = [I, I, I, P, P, P, P, I, I, P, D, I, P, P, P, P]
         lib.oracle_margins.restype = None
         lib.oracle_margins.argtypes = [I, P, P, D, I, I, I, I, P, P]
         lib.oracle_point_margins.restype = None
@@ -270,6 +270,7 @@ def render_points(p: Params, xs, ys, R2=None):
 class LossGrad:
     grad: np.ndarray       # [K, Pk]
     grad_abs: np.ndarray   # [K, Pk]  sum over pixels of |per-pixel term| (A_ref)
+    grad_opnd: np.ndarray  # [K, Pk]  operand scale B_ref (test tolerance only, see smoe_oracle.c)
     sse: float
     sse_clamped: float
     uncovered: int
@@ -294,14 +295,16 @@ def loss_grad(p: Params, target, rows=None, R2=None) -> LossGrad:
     mu, ch, lp, ex = _args(p)
     g = np.zeros((p.K, p.Pk))
     a = np.zeros((p.K, p.Pk))
+    b = np.zeros((p.K, p.Pk))
     st = np.zeros(3)
     _lib().oracle_loss_grad(p.K, p.C, p.order, _ptr(mu), _ptr(ch), _ptr(lp), _ptr(ex),
-                            H, W, _ptr(t), r0, r1, R2, _ptr(g), _ptr(a), _ptr(st))
-    return LossGrad(g, a, st[0], st[1], int(st[2]), C * H * W)
+                            H, W, _ptr(t), r0, r1, R2, _ptr(g), _ptr(a), _ptr(b), _ptr(st))
+    return LossGrad(g, a, b, st[0], st[1], int(st[2]), C * H * W)
 
 
-def grad_kernels(p: Params, target, sel, R2=None):
-    """Full-image gradient rows for the kernels in ``sel`` only."""
+def grad_kernels(p: Params, target, sel, R2=None, opnd=False):
+    """Full-image gradient rows for the kernels in ``sel`` only: (grad,
+    A_ref) or, with ``opnd``, (grad, A_ref, B_ref)."""
     t = _f64(target)
     C, H, W = t.shape
     R2 = R2_99() if R2 is None else R2
@@ -309,9 +312,10 @@ def grad_kernels(p: Params, target, sel, R2=None):
     mu, ch, lp, ex = _args(p)
     g = np.zeros((sel.size, p.Pk))
     a = np.zeros((sel.size, p.Pk))
+    b = np.zeros((sel.size, p.Pk))
     _lib().oracle_grad_kernels(p.K, p.C, p.order, _ptr(mu), _ptr(ch), _ptr(lp), _ptr(ex),
-                               H, W, _ptr(t), R2, sel.size, _ptr(sel), _ptr(g), _ptr(a))
-    return g, a
+                               H, W, _ptr(t), R2, sel.size, _ptr(sel), _ptr(g), _ptr(a), _ptr(b))
+    return (g, a, b) if opnd else (g, a)
 
 
 def margins(p: Params, H, W, out_H=None, out_W=None, R2=None):

@@ -215,8 +215,8 @@ void oracle_render_points(int K, int C, int order, const double *mu, const doubl
  *   dSigma/dl21 = [[0, l11],[l11, 2 l21]], dSigma/dl22 = [[0,0],[0, 2 l22]]. */
 static void add_pair_grad(int C, int order, const double *mu, const double *chol,
                           double log_pi, const double *e_j, double px, double py,
-                          const double *yv, double D, const double *ev, double R2,
-                          double *g, double *a)
+                          const double *yv, double D, const double *ev, const double *eva,
+                          double R2, double *g, double *a, double *b)
 {
     int E = 1 + 2 * order;
     double d2;
@@ -235,6 +235,16 @@ static void add_pair_grad(int C, int order, const double *mu, const double *chol
         G += ev[c] * (expert_value(e_j + c * E, order, dx, dy) - (g_head == 0 ? yv[c] : 0.0));
     if (g_head == 0) G /= D;
     double s = -0.5 * gn * G;
+    /* operand scale of the same term (b): every difference in it -- the
+     * residual y - t inside e_c and m_jc(x) - y_c inside G -- replaced by the
+     * sum of its operands' magnitudes, the scale of its rounding error in
+     * any finite-precision evaluation (forward error of a sum <= u * sum of
+     * |operands|).  Test tolerance scale only; not part of the gradient. */
+    double Gb = 0.0;
+    for (int c = 0; c < C; c++)
+        Gb += eva[c] * (fabs(expert_value(e_j + c * E, order, dx, dy)) + (g_head == 0 ? fabs(yv[c]) : 0.0));
+    if (g_head == 0) Gb /= D;
+    double sb = 0.5 * gn * Gb;
     double l11 = chol[0], l21 = chol[1], l22 = chol[2];
     double t[64];
     int n = 0;
@@ -256,6 +266,27 @@ static void add_pair_grad(int C, int order, const double *mu, const double *chol
         }
     }
     int P = n;
+    if (b) {
+        /* operand scale: gate-path terms with |s| -> sb, expert-path terms
+         * with |e_c| -> eva[c] */
+        double tb[6] = {2.0 * fabs(q1), 2.0 * fabs(q2), fabs(q1 * q1 * 2.0 * l11) + fabs(2.0 * q1 * q2 * l21),
+                        fabs(2.0 * q1 * q2 * l11) + fabs(q2 * q2 * 2.0 * l21), fabs(q2 * q2 * 2.0 * l22), 2.0};
+        for (int i = 0; i < 6; i++) b[i] += sb * tb[i];
+        int m = 6;
+        for (int c = 0; c < C; c++) {
+            double ew = eva[c] * w;
+            b[m++] += ew;
+            if (order == 1) {
+                b[m++] += ew * fabs(dx);
+                b[m++] += ew * fabs(dy);
+            }
+        }
+        if (order == 1)
+            for (int c = 0; c < C; c++) {
+                b[0] += eva[c] * w * fabs(e_j[c * E + 1]);
+                b[1] += eva[c] * w * fabs(e_j[c * E + 2]);
+            }
+    }
     if (order == 1) {
         double emx = 0.0, emy = 0.0;
         for (int c = 0; c < C; c++) {
@@ -279,13 +310,14 @@ static void add_pair_grad(int C, int order, const double *mu, const double *chol
 void oracle_loss_grad(int K, int C, int order, const double *mu, const double *chol,
                       const double *log_pi, const double *expert, int H, int W,
                       const double *target, int row0, int row1, double R2,
-                      double *grad, double *grad_abs, double *stats)
+                      double *grad, double *grad_abs, double *grad_opnd, double *stats)
 {
     int E = 1 + 2 * order, Pk = 6 + C * E;
     memset(grad, 0, sizeof(double) * (size_t)K * Pk);
     if (grad_abs) memset(grad_abs, 0, sizeof(double) * (size_t)K * Pk);
+    if (grad_opnd) memset(grad_opnd, 0, sizeof(double) * (size_t)K * Pk);
     double sse = 0.0, ssec = 0.0, unc = 0.0, N = (double)H * W * C;
-    double yv[8], ev[8];
+    double yv[8], ev[8], eva[8];
     for (int i = row0; i < row1; i++) {
         for (int jx = 0; jx < W; jx++) {
             double px = jx, py = i, D;
@@ -298,12 +330,14 @@ void oracle_loss_grad(int K, int C, int order, const double *mu, const double *c
                 double tc = t < 0 ? 0 : (t > 1 ? 1 : t);
                 ssec += (yc - tc) * (yc - tc);
                 ev[c] = 2.0 * r / N;                 /* dL/dy_c */
+                eva[c] = 2.0 * (fabs(yv[c]) + fabs(t)) / N;
             }
             if (!(D > 0.0)) { unc += 1.0; continue; } /* y = 0 is constant: no gradient */
             for (int j = 0; j < K; j++)
                 add_pair_grad(C, order, mu + 2 * j, chol + 3 * j, log_pi[j],
-                              expert + (size_t)j * C * E, px, py, yv, D, ev, R2,
-                              grad + (size_t)j * Pk, grad_abs ? grad_abs + (size_t)j * Pk : NULL);
+                              expert + (size_t)j * C * E, px, py, yv, D, ev, eva, R2,
+                              grad + (size_t)j * Pk, grad_abs ? grad_abs + (size_t)j * Pk : NULL,
+                              grad_opnd ? grad_opnd + (size_t)j * Pk : NULL);
         }
     }
     stats[0] = sse; stats[1] = ssec; stats[2] = unc;
@@ -316,13 +350,14 @@ void oracle_loss_grad(int K, int C, int order, const double *mu, const double *c
 void oracle_grad_kernels(int K, int C, int order, const double *mu, const double *chol,
                          const double *log_pi, const double *expert, int H, int W,
                          const double *target, double R2, int nsel, const int *sel,
-                         double *grad, double *grad_abs)
+                         double *grad, double *grad_abs, double *grad_opnd)
 {
     int E = 1 + 2 * order, Pk = 6 + C * E;
     double N = (double)H * W * C;
-    double yv[8], ev[8];
+    double yv[8], ev[8], eva[8];
     memset(grad, 0, sizeof(double) * (size_t)nsel * Pk);
     if (grad_abs) memset(grad_abs, 0, sizeof(double) * (size_t)nsel * Pk);
+    if (grad_opnd) memset(grad_opnd, 0, sizeof(double) * (size_t)nsel * Pk);
     for (int s = 0; s < nsel; s++) {
         int j = sel[s];
         int pb[4], tb[4];
@@ -333,11 +368,15 @@ void oracle_grad_kernels(int K, int C, int order, const double *mu, const double
                 double px = jx, py = i, D;
                 if (!(oracle_d2(mu + 2 * j, chol + 3 * j, px, py) <= R2)) continue;
                 eval_point(K, C, order, mu, chol, log_pi, expert, px, py, R2, yv, &D);
-                for (int c = 0; c < C; c++)
-                    ev[c] = 2.0 * (yv[c] - target[(size_t)c * H * W + (size_t)i * W + jx]) / N;
+                for (int c = 0; c < C; c++) {
+                    double t = target[(size_t)c * H * W + (size_t)i * W + jx];
+                    ev[c] = 2.0 * (yv[c] - t) / N;
+                    eva[c] = 2.0 * (fabs(yv[c]) + fabs(t)) / N;
+                }
                 add_pair_grad(C, order, mu + 2 * j, chol + 3 * j, log_pi[j],
-                              expert + (size_t)j * C * E, px, py, yv, D, ev, R2,
-                              grad + (size_t)s * Pk, grad_abs ? grad_abs + (size_t)s * Pk : NULL);
+                              expert + (size_t)j * C * E, px, py, yv, D, ev, eva, R2,
+                              grad + (size_t)s * Pk, grad_abs ? grad_abs + (size_t)s * Pk : NULL,
+                              grad_opnd ? grad_opnd + (size_t)s * Pk : NULL);
             }
     }
 }

@@ -41,8 +41,13 @@ constexpr int TILE = 16;                 // 16x16 blocks
 #ifndef SMOE_PRE_ATOM
 #define SMOE_PRE_ATOM 4                  // direct binning: count atomics in flight per kernel
 #endif
-#ifndef SMOE_ASM_LDS
-#define SMOE_ASM_LDS 1                   // backward: pixel seeds loaded through a 32-bit shared address
+#ifndef SMOE_RENDER_VEC
+#define SMOE_RENDER_VEC 1                // render epilogue: float4 row stores through shared memory
+#endif
+#ifndef SMOE_BWD_PACK
+#define SMOE_BWD_PACK 0                  // kernel-parallel backward: raw sums kept as f32x2 pixel-pair
+                                         // accumulators (bit 0: expert sums, bit 1: geometric sums);
+                                         // 0 (scalar) measured fastest: the pairs cost a resident CTA
 #endif
 constexpr int kFwdUnroll = SMOE_FWD_UNROLL;
 
@@ -52,6 +57,12 @@ __device__ __forceinline__ float4 lds128(unsigned a)
 {
     float4 v;
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float2 lds64(unsigned a)
+{
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
     return v;
 }
 __device__ __forceinline__ int lds32(unsigned a)
@@ -930,8 +941,11 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
     __shared__ float4 srec[BATCH * RS4];
     __shared__ int sid[BATCH];
     // per-lane backward seeds of the lane's pixel pair, packed by pixel:
-    // [warp][lane] = {(eD_0, eD_0'), (eD_1, eD_1')}, {(eD_2, eD_2'), (K, K')}
-    __shared__ float4 spix[MASKS ? 256 : 1];
+    // [warp][lane] = C = 1: {(eD_0, eD_0'), (K, K')}, {(x, y0), -}
+    //                C = 3: {(eD_0, eD_0'), (eD_1, eD_1')}, {(eD_2, eD_2'), (K, K')}, {(x, y0), -}
+    // with (x, y0) the lane's upper pixel in source coordinates
+    constexpr int NSEED = C == 1 ? 2 : 3;
+    __shared__ float4 spix[MASKS ? 128 * NSEED : 1];
     // per-warp kernel records of the pair list: {upper-pixel ballot, lower-pixel
     // ballot, kernel slot in the batch, entries before it}; a lane with either
     // pixel inside is one entry (a vertical pixel pair)
@@ -1065,17 +1079,65 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
 #pragma unroll
     for (int c = 0; c < C; c++) { y0[c] = N2[c].x * iD0; y1[c] = N2[c].y * iD1; }
 
-    if (!TRAIN) {
+    if (!TRAIN && !SMOE_RENDER_VEC) {
         size_t plane = (size_t)A.oH * A.oW;
         float *o0 = A.out + (size_t)py0 * A.oW + px, *o1 = A.out + (size_t)py1 * A.oW + px;
 #pragma unroll
         for (int c = 0; c < C; c++) {
-            if (A.accum != 0.f) {          // multi-model fusion: out += w y (Eq. 11)
+            if (A.accum != 0.f) {
                 if (v0) o0[c * plane] = fmaf(A.accum, y0[c], o0[c * plane]);
                 if (v1) o1[c * plane] = fmaf(A.accum, y1[c], o1[c * plane]);
             } else {
                 if (v0) o0[c * plane] = y0[c];
                 if (v1) o1[c * plane] = y1[c];
+            }
+        }
+        release();
+        return;
+    }
+    if (!TRAIN) {
+        // Render epilogue: the block's C x 16 x 16 outputs are staged in
+        // shared memory (the record batch buffer, free now) and written as
+        // coalesced float4 rows (st.global.v4: 16 B per thread, a block row is
+        // one 64-byte run).  Row stride 20 floats keeps the lane-pair layout
+        // of the staging writes free of bank conflicts and every float4
+        // 16-byte aligned.  Ragged edges and rasters whose width is not a
+        // multiple of 4 store the remaining pixels one by one.
+        constexpr int SR = 20;
+        static_assert(C * TILE * SR <= BATCH * RS4 * 4, "render staging exceeds the record buffer");
+        float *so = reinterpret_cast<float *>(srec);
+        const int cx = (warp & 1) * 8 + (lane & 7), cy = (warp >> 1) * 8 + (lane >> 3) * 2;
+        __syncthreads();                                  // every warp is done with the last batch
+#pragma unroll
+        for (int c = 0; c < C; c++) {
+            so[(c * TILE + cy) * SR + cx] = y0[c];
+            so[(c * TILE + cy + 1) * SR + cx] = y1[c];
+        }
+        __syncthreads();
+        const size_t plane = (size_t)A.oH * A.oW;
+        const bool vec = ((A.oW & 3) == 0) && ((reinterpret_cast<uintptr_t>(A.out) & 15) == 0);
+        const int x0 = tx * TILE, y0r = ty * TILE;
+        for (int i = threadIdx.x; i < C * TILE * 4; i += blockDim.x) {
+            const int c = i / (TILE * 4), r = (i >> 2) & (TILE - 1), q = i & 3;
+            const int y = y0r + r, x = x0 + 4 * q;
+            if (y >= A.oH || x >= A.oW) continue;
+            const float4 v = *reinterpret_cast<const float4 *>(so + (c * TILE + r) * SR + 4 * q);
+            float *o = A.out + c * plane + (size_t)y * A.oW + x;
+            if (vec && x + 3 < A.oW) {
+                float4 *o4 = reinterpret_cast<float4 *>(o);
+                if (A.accum != 0.f) {          // multi-model fusion: out += w y (Eq. 11)
+                    float4 a = *o4;
+                    a.x = fmaf(A.accum, v.x, a.x); a.y = fmaf(A.accum, v.y, a.y);
+                    a.z = fmaf(A.accum, v.z, a.z); a.w = fmaf(A.accum, v.w, a.w);
+                    *o4 = a;
+                } else {
+                    *o4 = v;
+                }
+            } else {
+                const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int e = 0; e < 4; e++)
+                    if (x + e < A.oW) o[e] = A.accum != 0.f ? fmaf(A.accum, vv[e], o[e]) : vv[e];
             }
         }
         release();
@@ -1115,11 +1177,15 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
         }
         if (lane == 0) { red[0][warp] = (double)sse; red[1][warp] = (double)ssec; red[2][warp] = (double)unc; }
         if (MASKS) {
-            float a0[4] = {0.f, 0.f, 0.f, K0}, a1[4] = {0.f, 0.f, 0.f, K1};
-#pragma unroll
-            for (int c = 0; c < C; c++) { a0[c] = eD0[c]; a1[c] = eD1[c]; }
-            spix[2 * threadIdx.x] = make_float4(a0[0], a1[0], a0[1], a1[1]);
-            spix[2 * threadIdx.x + 1] = make_float4(a0[2], a1[2], a0[3], a1[3]);
+            float4 *sp = spix + NSEED * threadIdx.x;
+            if (C == 1) {
+                sp[0] = make_float4(eD0[0], eD1[0], K0, K1);
+                sp[1] = make_float4(xs, ys0, 0.f, 0.f);
+            } else {
+                sp[0] = make_float4(eD0[0], eD1[0], eD0[C > 1 ? 1 : 0], eD1[C > 1 ? 1 : 0]);
+                sp[1] = make_float4(eD0[C > 2 ? 2 : 0], eD1[C > 2 ? 2 : 0], K0, K1);
+                sp[2] = make_float4(xs, ys0, 0.f, 0.f);
+            }
         }
         __syncthreads();
         if (threadIdx.x < 3) {
@@ -1162,7 +1228,7 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
                         acc[6 + c * E + 2] = fmaf(ge0, dy0, ge1 * dy1);
                     }
                 }
-                float sa = -0.5f * g0 * G0, sb = -0.5f * g1 * G1;
+                float sa = g0 * G0, sb = g1 * G1;          // gG (s = -gG/2, applied in k_adam)
                 float sv = fmaf(sa, w0, sb * w1);
                 acc[0] = (sa + sb) * u;
                 acc[1] = sv;
@@ -1194,8 +1260,7 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
     // entries; a lane accumulates the raw sums of the current kernel in
     // registers and flushes them with vector atomics when the kernel changes
     // and at the end of its range.
-    const float xw = (float)(tx * TILE + (warp & 1) * 8), yw = (float)(ty * TILE + (warp >> 1) * 8);
-    const float4 *spw_pix = spix + warp * 64;   // this warp's lanes' seeds
+    const float4 *spw_pix = spix + warp * 32 * NSEED;   // this warp's lanes' seeds
     unsigned spw_pix_s = (unsigned)__cvta_generic_to_shared(spw_pix);
     unsigned srec_s = (unsigned)__cvta_generic_to_shared(srec), sid_s = (unsigned)__cvta_generic_to_shared(sid);
     if (E == 3) {
@@ -1252,31 +1317,29 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
             }
             float4 *dst;
             float r[R::RS];
-            float bx, by;                       // quadrant origin - kernel centre
-            float acc[R::P];
+            // Raw sums of the current kernel, with gG = g G per
+            // pixel (s = dL/d(d^2) = -gG/2; the -1/2 is applied in k_adam):
+            //   gG u, gG v, gG u dx, gG v dx, gG v dy, gG, (g eD_c, g eD_c dx, g eD_c dy)_c
+            // kept as f32x2 pairs (upper, lower pixel of the lane) and summed
+            // across the pair only when flushed.
+            float2 A2[R::P];
 #pragma unroll
-            for (int i = 0; i < R::P; i++) acc[i] = 0.f;
+            for (int i = 0; i < R::P; i++) A2[i] = make_float2(0.f, 0.f);
             auto open_kernel = [&](int j) {
-                if (SMOE_ASM_LDS) {
-                    dst = reinterpret_cast<float4 *>(A.acc + (size_t)lds32(sid_s + 4u * j) * R::V);
+                dst = reinterpret_cast<float4 *>(A.acc + (size_t)lds32(sid_s + 4u * j) * R::V);
 #pragma unroll
-                    for (int q4 = 0; q4 < RS4; q4++) {
-                        const float4 f = lds128(srec_s + 16u * (j * RS4 + q4));
-                        r[4 * q4] = f.x; r[4 * q4 + 1] = f.y; r[4 * q4 + 2] = f.z; r[4 * q4 + 3] = f.w;
-                    }
-                } else {
-                    dst = reinterpret_cast<float4 *>(A.acc + (size_t)sid[j] * R::V);
-                    load_rec(j, r);
+                for (int q4 = 0; q4 < RS4; q4++) {
+                    const float4 f = lds128(srec_s + 16u * (j * RS4 + q4));
+                    r[4 * q4] = f.x; r[4 * q4 + 1] = f.y; r[4 * q4 + 2] = f.z; r[4 * q4 + 3] = f.w;
                 }
-                bx = xw - r[0];
-                by = yw - r[1];
             };
             auto flush = [&] {
 #pragma unroll
                 for (int q4 = 0; q4 < (R::P + 3) / 4; q4++) {
                     float t4[4];
 #pragma unroll
-                    for (int k4 = 0; k4 < 4; k4++) t4[k4] = (4 * q4 + k4 < R::P) ? acc[4 * q4 + k4] : 0.f;
+                    for (int k4 = 0; k4 < 4; k4++)
+                        t4[k4] = (4 * q4 + k4 < R::P) ? A2[4 * q4 + k4].x + A2[4 * q4 + k4].y : 0.f;
                     atomicAdd(dst + q4, make_float4(t4[0], t4[1], t4[2], t4[3]));
                 }
             };
@@ -1286,7 +1349,7 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
                     // kernel switch: flush this kernel's sums, open the next record
                     flush();
 #pragma unroll
-                    for (int i = 0; i < R::P; i++) acc[i] = 0.f;
+                    for (int i = 0; i < R::P; i++) A2[i] = make_float2(0.f, 0.f);
                     kr = skr[warp][++ra];
                     m = kr.x | kr.y;
                     open_kernel((int)kr.z);
@@ -1294,30 +1357,38 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
                 const unsigned lb = m & (0u - m);       // lowest listed lane
                 m ^= lb;
                 const int l = 31 - __clz(lb);
-                const bool g0 = (kr.x & lb) != 0u, g1 = (kr.y & lb) != 0u;
-                // this pair's contribution to the raw sums (a pixel outside the ellipse: g = 0)
-                float4 pa, pb;
-                if (SMOE_ASM_LDS) {
-                    const unsigned a = spw_pix_s + ((unsigned)l << 5);   // + 32 l bytes
-                    pa = lds128(a);
-                    pb = lds128(a + 16u);
+                const bool h0 = (kr.x & lb) != 0u, h1 = (kr.y & lb) != 0u;
+                // this pair's seeds and coordinates (a pixel outside the ellipse: g = 0)
+                const unsigned a = spw_pix_s + (unsigned)l * (16u * NSEED);
+                float2 ed[C], Kp, xy;
+                if (C == 1) {
+                    const float4 p0 = lds128(a), p1 = lds128(a + 16u);
+                    ed[0] = make_float2(p0.x, p0.y);
+                    Kp = make_float2(p0.z, p0.w);
+                    xy = make_float2(p1.x, p1.y);
                 } else {
-                    pa = spw_pix[2 * l];
-                    pb = spw_pix[2 * l + 1];
+                    const float4 p0 = lds128(a), p1 = lds128(a + 16u);
+                    const float2 p2 = lds64(a + 32u);
+                    ed[0] = make_float2(p0.x, p0.y);
+                    ed[C > 1 ? 1 : 0] = make_float2(p0.z, p0.w);
+                    ed[C > 2 ? 2 : 0] = make_float2(p1.x, p1.y);
+                    Kp = make_float2(p1.z, p1.w);
+                    xy = p2;
                 }
-                const float dx = bx + (float)(l & 7);
-                const float yl = by + (float)((l >> 3) * 2);
-                const float2 dy = make_float2(yl, yl + 1.0f);
+                const float2 dd = __fadd2_rn(xy, make_float2(-r[0], -r[1]));   // (dx, dy of the upper pixel)
+                const float dx = dd.x;
+                const float2 dy = __fadd2_rn(make_float2(dd.y, dd.y), make_float2(0.f, 1.0f));
                 const float u = r[2] * dx;
                 const float bdx = r[3] * dx;
                 const float2 v = __ffma2_rn(make_float2(r[4], r[4]), dy, make_float2(bdx, bdx));
                 const float uu = u * u;
                 const float2 qd = __ffma2_rn(v, v, make_float2(uu, uu));
                 const float2 ea = __ffma2_rn(qd, make_float2(-0.5f * LOG2E, -0.5f * LOG2E), make_float2(r[5], r[5]));
-                const float2 g = make_float2(g0 ? ex2_approx(ea.x) : 0.f, g1 ? ex2_approx(ea.y) : 0.f);
-                const float2 eda[4] = {make_float2(pa.x, pa.y), make_float2(pa.z, pa.w),
-                                       make_float2(pb.x, pb.y), make_float2(pb.z, pb.w)};
-                float2 Gs = make_float2(-eda[3].x, -eda[3].y);
+                const float2 g = make_float2(h0 ? ex2_approx(ea.x) : 0.f, h1 ? ex2_approx(ea.y) : 0.f);
+                // packed sums: one FFMA2/FADD2 per pair; scalar sums (in .x;
+                // .y stays 0): the pair's two products added first
+                constexpr bool PE = (SMOE_BWD_PACK & 1) != 0, PG = (SMOE_BWD_PACK & 2) != 0;
+                float2 Gs = make_float2(-Kp.x, -Kp.y);
 #pragma unroll
                 for (int c = 0; c < C; c++) {
                     float2 mc = make_float2(r[6 + c * E], r[6 + c * E]);
@@ -1325,25 +1396,47 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
                         const float mb = fmaf(r[6 + c * E + 1], dx, r[6 + c * E]);
                         mc = __ffma2_rn(make_float2(r[6 + c * E + 2], r[6 + c * E + 2]), dy, make_float2(mb, mb));
                     }
-                    Gs = __ffma2_rn(eda[c], mc, Gs);
-                    const float2 ge = __fmul2_rn(g, eda[c]);
-                    const float gsum = ge.x + ge.y;
-                    acc[6 + c * E] += gsum;
+                    Gs = __ffma2_rn(ed[c], mc, Gs);
+                    float2 &am = A2[6 + c * E];
                     if (E == 3) {
-                        acc[6 + c * E + 1] = fmaf(gsum, dx, acc[6 + c * E + 1]);
-                        acc[6 + c * E + 2] = fmaf(ge.x, dy.x, fmaf(ge.y, dy.y, acc[6 + c * E + 2]));
+                        const float2 ge = __fmul2_rn(g, ed[c]);
+                        float2 &ax = A2[6 + c * E + 1], &ay = A2[6 + c * E + 2];
+                        if (PE) {
+                            am = __fadd2_rn(am, ge);
+                            ax = __ffma2_rn(ge, make_float2(dx, dx), ax);
+                            ay = __ffma2_rn(ge, dy, ay);
+                        } else {
+                            const float gs = ge.x + ge.y;
+                            am.x += gs;
+                            ax.x = fmaf(gs, dx, ax.x);
+                            ay.x = fmaf(ge.x, dy.x, fmaf(ge.y, dy.y, ay.x));
+                        }
+                    } else if (PE) {
+                        am = __ffma2_rn(g, ed[c], am);
+                    } else {
+                        const float2 ge = __fmul2_rn(g, ed[c]);
+                        am.x += ge.x + ge.y;
                     }
                 }
-                const float2 sg = __fmul2_rn(__fmul2_rn(make_float2(-0.5f, -0.5f), g), Gs);
-                const float ssum = sg.x + sg.y;
-                const float2 sv = __fmul2_rn(sg, v);
-                const float svsum = sv.x + sv.y;
-                acc[0] = fmaf(ssum, u, acc[0]);
-                acc[1] += svsum;
-                acc[2] = fmaf(ssum, u * dx, acc[2]);
-                acc[3] = fmaf(svsum, dx, acc[3]);
-                acc[4] = fmaf(sv.x, dy.x, fmaf(sv.y, dy.y, acc[4]));
-                acc[5] += ssum;
+                const float2 gG = __fmul2_rn(g, Gs);
+                const float2 sv = __fmul2_rn(gG, v);
+                const float udx = u * dx;
+                if (PG) {
+                    A2[0] = __ffma2_rn(gG, make_float2(u, u), A2[0]);
+                    A2[1] = __fadd2_rn(A2[1], sv);
+                    A2[2] = __ffma2_rn(gG, make_float2(udx, udx), A2[2]);
+                    A2[3] = __ffma2_rn(sv, make_float2(dx, dx), A2[3]);
+                    A2[4] = __ffma2_rn(sv, dy, A2[4]);
+                    A2[5] = __fadd2_rn(A2[5], gG);
+                } else {
+                    const float gs = gG.x + gG.y, vs = sv.x + sv.y;
+                    A2[0].x = fmaf(gs, u, A2[0].x);
+                    A2[1].x += vs;
+                    A2[2].x = fmaf(gs, udx, A2[2].x);
+                    A2[3].x = fmaf(vs, dx, A2[3].x);
+                    A2[4].x = fmaf(sv.x, dy.x, fmaf(sv.y, dy.y, A2[4].x));
+                    A2[5].x += gs;
+                }
             }
             flush();
         }
@@ -1388,13 +1481,16 @@ k_raster(RasterArgs A)
 // MODE 0 (step):   raw sums -> parameter gradients -> Adam -> clamp; reset sums
 // MODE 1 (grad):   raw sums -> parameter gradients -> grad_out; reset sums
 // MODE 2 (apply):  grad_in -> Adam -> clamp
-// Chain rule (DESIGN.md appendix A): with raw Su, Sv, Sux, Svx, Svy, Ss, gm,
-//   dL/dmu_x = -2 (a Su + b Sv) - sum_c Wx_c gm_c
-//   dL/dmu_y = -2 c Sv          - sum_c Wy_c gm_c
-//   dL/dl11  = -2 (a^2 Sux + a b Svx)
-//   dL/dl21  = -2 a c Svx
-//   dL/dl22  = -2 (b c Svx + c^2 Svy)
-//   dL/dlog_pi = -2 Ss
+// Chain rule (DESIGN.md appendix A): the raster sums, per
+// kernel, Tu = sum gG u, Tv = sum gG v, Tux = sum gG u dx, Tvx = sum gG v dx,
+// Tvy = sum gG v dy, Tg = sum gG and gm_c = sum g eD_c (pixel terms with
+// gG = g G = -2 s, s = dL/d(d^2)), so
+//   dL/dmu_x = a Tu + b Tv - sum_c Wx_c gm_c
+//   dL/dmu_y = c Tv        - sum_c Wy_c gm_c
+//   dL/dl11  = a^2 Tux + a b Tvx
+//   dL/dl21  = a c Tvx
+//   dL/dl22  = b c Tvx + c^2 Tvy
+//   dL/dlog_pi = Tg
 // Adam (Q9): beta1 0.9, beta2 0.999, eps 1e-8 outside the sqrt,
 // bias-corrected; clamp l11, l22 >= 1e-3.  Moments are stored
 // parameter-major m[Pk][K] so every access is coalesced.
@@ -1517,7 +1613,7 @@ k_adam(AdamCommon cm, ParamsMut p, float *__restrict__ acc, const float *__restr
                 if (v >= 6) {
                     g = raw[v];
                 } else if (v == 5) {
-                    g = -2.f * raw[5];
+                    g = raw[5];
                 } else {
                     const float l11 = prm[2], l21 = prm[3], l22 = prm[4];
                     const float a = 1.0f / l11, c = 1.0f / l22;
@@ -1528,13 +1624,13 @@ k_adam(AdamCommon cm, ParamsMut p, float *__restrict__ acc, const float *__restr
 #pragma unroll
                             for (int ch = 0; ch < C; ch++) ex = fmaf(prm[6 + ch * E + 1 + v], raw[6 + ch * E], ex);
                         }
-                        g = (v == 0 ? -2.f * fmaf(a, raw[0], b * raw[1]) : -2.f * c * raw[1]) - ex;
+                        g = (v == 0 ? fmaf(a, raw[0], b * raw[1]) : c * raw[1]) - ex;
                     } else if (v == 2) {
-                        g = -2.f * fmaf(a * a, raw[2], a * b * raw[3]);
+                        g = fmaf(a * a, raw[2], a * b * raw[3]);
                     } else if (v == 3) {
-                        g = -2.f * a * c * raw[3];
+                        g = a * c * raw[3];
                     } else {
-                        g = -2.f * fmaf(b * c, raw[3], c * c * raw[4]);
+                        g = fmaf(b * c, raw[3], c * c * raw[4]);
                     }
                 }
             }
@@ -1624,12 +1720,12 @@ k_adam_kt(AdamCommon cm, ParamsMut p, float *__restrict__ acc, const float *__re
                     ex_y = fmaf(prm[6 + ch * E + 2], raw[6 + ch * E], ex_y);
                 }
             }
-            g[0] = -2.f * fmaf(a, raw[0], b * raw[1]) - ex_x;
-            g[1] = -2.f * c * raw[1] - ex_y;
-            g[2] = -2.f * fmaf(a * a, raw[2], a * b * raw[3]);
-            g[3] = -2.f * a * c * raw[3];
-            g[4] = -2.f * fmaf(b * c, raw[3], c * c * raw[4]);
-            g[5] = -2.f * raw[5];
+            g[0] = fmaf(a, raw[0], b * raw[1]) - ex_x;
+            g[1] = c * raw[1] - ex_y;
+            g[2] = fmaf(a * a, raw[2], a * b * raw[3]);
+            g[3] = a * c * raw[3];
+            g[4] = fmaf(b * c, raw[3], c * c * raw[4]);
+            g[5] = raw[5];
 #pragma unroll
             for (int i = 6; i < P; i++) g[i] = raw[i];
             float4 *ap = reinterpret_cast<float4 *>(acc) + (size_t)k * (R::V / 4);

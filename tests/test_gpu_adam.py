@@ -122,8 +122,11 @@ def test_apply_trajectory_matches_oracle_adam(C, order, K):
     assert (np.abs(op.chol[:, 0] - 1e-3) < 1e-12).any()          # the clamp engaged
     m1, m2, tt = h.get_adam()
     assert tt == T
-    np.testing.assert_allclose(m1.numpy(), opt.m1, rtol=1e-5, atol=1e-12)
-    np.testing.assert_allclose(m2.numpy(), opt.m2, rtol=1e-5, atol=1e-20)
+    # fp32 accumulation of the moments: relative to the largest term of the
+    # (possibly cancelling) sum, per component
+    gmax = np.abs(G).max(axis=0).astype(np.float64)
+    assert (np.abs(m1.numpy() - opt.m1) <= 1e-5 * np.abs(opt.m1) + 1e-6 * gmax).all()
+    assert (np.abs(m2.numpy() - opt.m2) <= 1e-5 * np.abs(opt.m2) + 1e-6 * gmax ** 2).all()
 
 
 @pytest.mark.parametrize("K", [300, 20_000])

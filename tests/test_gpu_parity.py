@@ -95,7 +95,7 @@ def test_binning_all_binners(binner, monkeypatch):
         for _ in range(2):                        # eager (calibrating) pass, then graph replay
             g, _ = h.grad(p, target)
         acc = g.clone() if acc is None else acc + g
-    assert_grads(acc.cpu().numpy(), lg.grad, lg.grad_abs)
+    assert_grads(acc.cpu().numpy(), lg.grad, lg.grad_abs, b_ref=lg.grad_opnd)
 
 
 def test_binning_kodak_density_and_determinism():
@@ -135,23 +135,33 @@ def test_binning_large_bucket_merge_path():
 
 @pytest.mark.parametrize("mode", [0, 1])
 def test_grad_parity_bucket_over_2048(mode):
-    """Gradients of a block whose list (5000 kernels) exceeds the in-smem
-    sort (2048: CTA merge sort through global scratch) and spans 40 record
+    """Gradients of a block whose list (2500 kernels) exceeds the in-smem
+    sort (2048: CTA merge sort through global scratch) and spans 20 record
     batches of 128 (the kernel-parallel backward rebuilds its ballot records
     per batch)."""
-    H, W, K = 32, 32, 5000
+    H, W, K = 32, 32, 2500
     g = np.random.default_rng(0)
-    pool = synth.aniso_pool(H, W, 1, K, 9, l_range=(0.3, 0.6), shear=0.1, log_pi_sd=0.3)
-    pool.mu[:] = g.uniform(18.2, 29.8, (K, 2)).astype(np.float32)
+    # sigma 0.35-0.5 px spread over the whole block: each kernel covers ~4
+    # pixel centres and ~60 kernels cover a pixel (the fp32 forward sums D
+    # and N over them in list order; the 1e-5 A_ref floor assumes no more
+    # than ~1e2 such terms)
+    # order).  A kernel here covers only 1-3 pixel centres, so its gradient
+    # is a sum of a few terms, each proportional to its pixel's residual
+    # e = 2(y - t)/(HWC): the target sits at 1 while the experts stay in
+    # [0, 0.5], so no residual is near 0 (where the fp32 rounding of y,
+    # ~1e-7 of the gate sum, would be a large fraction of e and of the term)
+    pool = synth.aniso_pool(H, W, 1, K, 9, l_range=(0.35, 0.5), shear=0.05, log_pi_sd=0.3)
+    pool.mu[:] = g.uniform(17.6, 30.4, (K, 2)).astype(np.float32)
+    pool.expert *= 0.5
     pool = conditioned(pool, H, W)
-    target = synth.image(H, W, 1, 10)
+    target = np.ones((1, H, W), np.float32) - 0.02 * synth.image(H, W, 1, 10)
     h = smoe.SMoE(K, H, W, 1, 0, backward_mode=mode)
     rng, _, _ = h.bin(dev_pool(pool))
     assert int((rng[1:] - rng[:-1]).max()) > 2048
     gr, sums = h.grad(dev_pool(pool), torch.as_tensor(target).cuda())
     lg = O.loss_grad(opar(pool), target.astype(np.float64))
     assert abs(float(sums[0]) - lg.sse) <= 1e-5 * lg.sse
-    assert_grads(gr.cpu().numpy(), lg.grad, lg.grad_abs)
+    assert_grads(gr.cpu().numpy(), lg.grad, lg.grad_abs, b_ref=lg.grad_opnd)
 
 
 @pytest.mark.parametrize("direct_max", ["", "32768"])
@@ -258,7 +268,7 @@ def test_grad_parity(H, W, C, K, order, mode):
     assert abs(s[0] - lg.sse) <= 1e-5 * lg.sse
     assert abs(s[1] - lg.sse_clamped) <= 1e-5 * lg.sse_clamped
     assert int(s[2]) == lg.uncovered
-    assert_grads(g.cpu().numpy(), lg.grad, lg.grad_abs)
+    assert_grads(g.cpu().numpy(), lg.grad, lg.grad_abs, b_ref=lg.grad_opnd)
 
 
 @pytest.mark.parametrize("mode", [0, 1])
@@ -275,7 +285,7 @@ def test_grad_parity_dense_buckets(mode):
     g, sums = h.grad(dev_pool(pool), torch.as_tensor(target).cuda())
     lg = O.loss_grad(opar(pool), target.astype(np.float64))
     assert abs(float(sums[0]) - lg.sse) <= 1e-5 * lg.sse
-    assert_grads(g.cpu().numpy(), lg.grad, lg.grad_abs)
+    assert_grads(g.cpu().numpy(), lg.grad, lg.grad_abs, b_ref=lg.grad_opnd)
 
 
 def test_grad_host_buffers_and_uncovered():
@@ -289,7 +299,7 @@ def test_grad_host_buffers_and_uncovered():
     assert sums[3] == 0.0
     lg = O.loss_grad(opar(pool), target.astype(np.float64))
     assert lg.uncovered > 0 and int(sums[2]) == lg.uncovered
-    assert_grads(g, lg.grad, lg.grad_abs)
+    assert_grads(g, lg.grad, lg.grad_abs, b_ref=lg.grad_opnd)
 
 
 def test_band_additivity_on_one_gpu():
@@ -309,7 +319,7 @@ def test_band_additivity_on_one_gpu():
         sacc += s
     h.set_band(0, 0)
     lg = O.loss_grad(opar(pool), target.cpu().numpy().astype(np.float64))
-    assert_grads(acc.cpu().numpy(), lg.grad, lg.grad_abs, what="band sum")
+    assert_grads(acc.cpu().numpy(), lg.grad, lg.grad_abs, b_ref=lg.grad_opnd, what="band sum")
     assert abs(float(sacc[0]) - float(fs[0])) < 1e-9 * float(fs[0])
 
 
@@ -445,8 +455,8 @@ def test_kodak_full_size_sampled_parity():
     assert_pixels(y[:, iy, ix].T, y_ref)
     grad, _ = h.grad(p, torch.as_tensor(target).cuda())
     sel = g.choice(K, 16, replace=False)
-    g_ref, a_ref = O.grad_kernels(op, target.astype(np.float64), sel)
-    assert_grads(grad.cpu().numpy()[sel], g_ref, a_ref)
+    g_ref, a_ref, b_ref = O.grad_kernels(op, target.astype(np.float64), sel, opnd=True)
+    assert_grads(grad.cpu().numpy()[sel], g_ref, a_ref, b_ref=b_ref)
 
 
 # -------------------------------------------- NEXT rows f1 / f2 on the GPU --
@@ -488,7 +498,7 @@ def test_rbf_head_parity(C, order, mode):
         lg = O.loss_grad(opar(pool), target.astype(np.float64))
     assert_pixels(y, y_ref)
     assert abs(float(sums[0]) - lg.sse) <= 1e-5 * lg.sse
-    assert_grads(g.cpu().numpy(), lg.grad, lg.grad_abs)
+    assert_grads(g.cpu().numpy(), lg.grad, lg.grad_abs, b_ref=lg.grad_opnd)
 
 
 def test_dense_global_model_parity():
@@ -506,7 +516,7 @@ def test_dense_global_model_parity():
     assert_pixels(y, y_ref)
     g, _ = h.grad(dev_pool(pool), torch.as_tensor(target).cuda())
     lg = O.loss_grad(opar(pool), target.astype(np.float64), R2=float("inf"))
-    assert_grads(g.cpu().numpy(), lg.grad, lg.grad_abs)
+    assert_grads(g.cpu().numpy(), lg.grad, lg.grad_abs, b_ref=lg.grad_opnd)
 
 
 # ------------------------------------------------------ NEXT row f3 (GPU) --
@@ -560,7 +570,7 @@ def test_degenerate_image_shapes(H, W):
     gr, sums = h.grad(dev_pool(pool), torch.as_tensor(target).cuda())
     lg = O.loss_grad(opar(pool), target.astype(np.float64))
     assert abs(float(sums[0]) - lg.sse) <= 1e-5 * max(lg.sse, 1e-12)
-    assert_grads(gr.cpu().numpy(), lg.grad, lg.grad_abs)
+    assert_grads(gr.cpu().numpy(), lg.grad, lg.grad_abs, b_ref=lg.grad_opnd)
 
 
 def test_single_kernel_and_image_covering_kernel():
@@ -583,7 +593,7 @@ def test_single_kernel_and_image_covering_kernel():
     gr, _ = h2.grad(dev_pool(big), torch.as_tensor(target).cuda())
     lg = O.loss_grad(opar(big), target.astype(np.float64))
     assert lg.uncovered == 0
-    assert_grads(gr.cpu().numpy(), lg.grad, lg.grad_abs)
+    assert_grads(gr.cpu().numpy(), lg.grad, lg.grad_abs, b_ref=lg.grad_opnd)
 
 
 def test_band_with_kernel_parallel_backward_and_graph_replay():
@@ -605,7 +615,7 @@ def test_band_with_kernel_parallel_backward_and_graph_replay():
         acc += g
     h.set_band(0, 0)
     lg = O.loss_grad(opar(pool), target.cpu().numpy().astype(np.float64))
-    assert_grads(acc.cpu().numpy(), lg.grad, lg.grad_abs, what="band sum (kernel-parallel)")
+    assert_grads(acc.cpu().numpy(), lg.grad, lg.grad_abs, b_ref=lg.grad_opnd, what="band sum (kernel-parallel)")
 
 
 def test_host_target_pipelined_steps_match_device_target():
@@ -683,8 +693,8 @@ def _sampled_parity(cfg, n_px=1500, n_kern=8, sr=None, seed=0):
     inside = np.flatnonzero((tb[:, 0] > 0) & (tb[:, 2] > 0) & (tb[:, 1] < (W - 1) // 16) &
                             (tb[:, 3] < (H - 1) // 16))
     sel = np.sort(g.choice(inside, n_kern, replace=False))
-    g_ref, a_ref = O.grad_kernels(op, target.astype(np.float64), sel)
-    assert_grads(grad.cpu().numpy()[sel], g_ref, a_ref, what=f"{cfg} sampled kernels")
+    g_ref, a_ref, b_ref = O.grad_kernels(op, target.astype(np.float64), sel, opnd=True)
+    assert_grads(grad.cpu().numpy()[sel], g_ref, a_ref, b_ref=b_ref, what=f"{cfg} sampled kernels")
 
 
 def test_config3_div2k_full_size_sampled():

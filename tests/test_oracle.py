@@ -615,3 +615,25 @@ def test_point_margins_against_numpy():
     v = L @ np.array([np.cos(0.7), np.sin(0.7)]) * np.sqrt(R2)     # on the ellipse
     assert O.point_margins(one, [5.0 + v[0]], [7.0 + v[1]])[0] < 1e-12
     assert abs(O.point_margins(one, [5.0], [7.0])[0] - R2) < 1e-12
+
+
+def test_operand_scale_bounds_term_scale():
+    """B_ref (O.loss_grad grad_opnd, a tolerance scale) replaces every
+    difference inside a per-pixel term by the sum of its operands'
+    magnitudes, so it bounds A_ref (sum of |terms|) from above, and the two
+    coincide for the expert terms of a model whose residuals cannot cancel
+    (target 0, non-negative experts)."""
+    H, W = 20, 24
+    pool = synth.aniso_pool(H, W, 3, 30, 31, order=1, log_pi_sd=0.3)
+    p = pool_params(pool)
+    t = synth.image(H, W, 3, 32).astype(np.float64)
+    lg = O.loss_grad(p, t)
+    assert (lg.grad_opnd >= lg.grad_abs * (1 - 1e-12)).all()
+    g, a, b = O.grad_kernels(p, t, np.arange(0, 30, 7), opnd=True)
+    np.testing.assert_allclose(b, lg.grad_opnd[0:30:7], rtol=1e-12)
+    q = p.copy()
+    q.expert[:, :, 1:] = 0.0
+    q.expert[:, :, 0] = np.abs(q.expert[:, :, 0])
+    lz = O.loss_grad(q, np.zeros((3, H, W)))
+    m = slice(6, None, 3)                         # m_c components: g eD_c, no inner difference
+    np.testing.assert_allclose(lz.grad_opnd[:, m], lz.grad_abs[:, m], rtol=1e-12, atol=0)
