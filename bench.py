@@ -220,6 +220,71 @@ def run_mm(args):
     return 0
 
 
+def run_project(args):
+    """Per-rank projection of the multi-GPU fit on ONE GPU:
+    for N ranks, time rank r's share of a step -- smoe_grad on its band of
+    block rows (band-local preprocess + binning + raster) and smoe_apply_ex
+    on its kernel shard -- with CUDA events after warm-up, L2 flushed between
+    calls, for the first, a middle and the last band.  The collectives
+    (reduce-scatter of K x Pk fp32, all-reduce of 4 doubles, all-gather of
+    the parameters) cannot run on one GPU: their time is modelled as ring
+    transfers at 900 GB/s per direction plus 10 us latency each, and stated
+    as a model, not a measurement."""
+    import torch
+    from paper_2510_05814_b200 import smoe, synth
+    from paper_2510_05814_b200.dist import band_rows, shard_rows
+    cfg = dict(synth.CONFIGS[args.config])
+    C, H, W, K, order = cfg["C"], cfg["H"], cfg["W"], cfg["K"], cfg["order"]
+    target, _, pool = synth.workload(args.config)
+    dev = torch.device("cuda", 0)
+    tgt = torch.as_tensor(target).to(dev)
+    params = smoe.Params.from_numpy(pool, dev)
+    flush = L2Flush(dev)
+    ny = (H + 15) // 16
+    E = 1 + 2 * order
+    Pk = 6 + C * E
+    out = {"metric": "per-rank step projection", "config": config_dict(args.config, 1), "ranks": {}}
+
+    def timed(fn, n):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+        for i in range(n):
+            flush()
+            ev[i][0].record()
+            fn()
+            ev[i][1].record()
+        torch.cuda.synchronize()
+        return sorted(a.elapsed_time(b) for a, b in ev)[n // 2]
+
+    for N in [int(x) for x in args.project.split(",")]:
+        rows = {}
+        k0, k1, Ks = shard_rows(K, 0, N)
+        grad_sh = torch.zeros((k1 - k0, Pk), dtype=torch.float32, device=dev)
+        for r in sorted({0, N // 2, N - 1}):
+            b0, b1 = band_rows(ny, r, N)
+            h = smoe.SMoE(K, H, W, C, order)
+            if N > 1:
+                h.set_band(b0, b1)
+            g = torch.empty((K, Pk), dtype=torch.float32, device=dev)
+            sums = torch.empty(4, dtype=torch.float64, device=dev)
+            for _ in range(args.warmup):
+                h.grad(params, tgt, g, sums)
+            grad_ms = timed(lambda: h.grad(params, tgt, g, sums), args.steps)
+            p2 = params.clone()
+            apply_ms = timed(lambda: h.apply(p2, grad_sh, smoe.LR(0, 0, 0, 0, 0), k0, k1), args.steps)
+            rows[f"rank{r}"] = {"band_rows": [b0, b1], "grad_ms": grad_ms, "apply_ms": apply_ms,
+                                "pairs": h.sync().pairs}
+            h.close()
+        bytes_rs = K * Pk * 4
+        bytes_ag = K * Pk * 4
+        comm_ms = 0.0 if N == 1 else (2 * (N - 1) / N * (bytes_rs + bytes_ag) / 2 / 900e9 * 1e3 + 3 * 0.010)
+        worst = max(v["grad_ms"] + v["apply_ms"] for v in rows.values())
+        out["ranks"][N] = {"per_band": rows, "worst_rank_compute_ms": worst, "comm_model_ms": comm_ms,
+                           "projected_ms_per_step": worst + comm_ms,
+                           "projected_it_s": 1e3 / (worst + comm_ms)}
+    print(json.dumps(out))
+    return 0
+
+
 def config_dict(name, world):
     from paper_2510_05814_b200 import synth
     c = synth.CONFIGS[name]
@@ -306,8 +371,14 @@ def main():
                     help="with --mm: segmentation-guided init (SURVEY f4) at this threshold (0-255 scale)")
     ap.add_argument("--mm", type=int, default=0,
                     help="MM-RSMoE (SURVEY f3): fit this many hypotheses concurrently and report the fused denoising")
+    ap.add_argument("--box-modes", action="store_true",
+                    help="after the fit: list pairs and time the gradient pass under each box mode (reading Q4)")
+    ap.add_argument("--project", default="",
+                    help="comma-separated rank counts: per-rank projection of the banded fit on one GPU")
     args = ap.parse_args()
     assert args.warmup >= 3, "at least 3 warm-up steps"
+    if args.project:
+        return run_project(args)
     if args.impl == "reference":
         return run_reference(args)
     if args.mm:
@@ -425,6 +496,30 @@ def main():
         step(t)
     st_fit = h.sync()
 
+    # box modes (reading Q4) on the fitted pool: pairs listed and the train
+    # raster's time per mode (pixels and gradients are mode-independent)
+    box_modes = None
+    if args.box_modes and world == 1:
+        box_modes = {}
+        gm = torch.empty((K, 6 + C * (1 + 2 * order)), dtype=torch.float32, device=dev)
+        sm = torch.empty(4, dtype=torch.float64, device=dev)
+        for mode in ("square", "aabb", "exact"):
+            hm = smoe.SMoE(K, H, W, C, order, device=local, box_mode=mode)
+            for _ in range(3):
+                hm.grad(params, tgt, gm, sm)
+            n = min(args.steps, 100)
+            hm.profile_begin(8 * n + 16)
+            for _ in range(n):
+                if flush is not None:
+                    flush()
+                hm.grad(params, tgt, gm, sm)
+            kt, _ = hm.profile_end()
+            stm = hm.sync()
+            box_modes[mode] = {"pairs": stm.pairs, "avg_kernels_per_block": stm.pairs / max(stm.n_tiles, 1),
+                               "kernel_ms": {k2: v[0] / v[1] for k2, v in kt.items()},
+                               "grad_ms": sum(v[0] for v in kt.values()) / n}
+            hm.close()
+
     # roofline of the dominant kernel (raster: FP32 pipe)
     peaks, peak_kind = load_peaks()
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
@@ -442,11 +537,15 @@ def main():
         V = 8 if Pk <= 8 else 16
         hbm = peaks.get("hbm_gbs", 6554.2)
         pairs = st.pairs
-        pre_bytes = K * (4 * Pk + 16 + RSb) + 4 * pairs
+        two = "k_emit" in breakdown
+        pre_bytes = K * (4 * Pk + 16 + RSb) + (0 if two else 4 * pairs)
+        emit_bytes = K * (4 + 16) + 4 * pairs
         adam_bytes = K * (24 * Pk + 8 * V)
         for name, b, what in (("k_preprocess", pre_bytes, f"read params {4 * Pk} B + write tile box 16 B + record "
-                                                        f"{RSb} B per kernel, + 4 B kernel id per pair (count "
-                                                        f"atomics are L2 traffic, not counted)"),
+                                                        f"{RSb} B per kernel" + ("" if two else ", + 4 B kernel id per "
+                                                        "pair (count atomics are L2 traffic, not counted)")),
+                              ("k_emit", emit_bytes, "read the spatial order 4 B + tile box 16 B per kernel, write "
+                                                     "4 B kernel id per pair (one count atomic per CTA and block)"),
                               ("k_adam", adam_bytes, f"per kernel: params, m1, m2 read + write ({24 * Pk} B), raw "
                                                      f"sums read + zeroed ({8 * V} B)")):
             if name in breakdown and breakdown[name] > 0:
@@ -563,7 +662,7 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": dict(config_dict(args.config, world), **({"K": K, "K_override": True} if args.K else {})),
             "render": render, "roofline": roof, "kernel_rooflines": kernels, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": launches, "clocks": clk,
+            "gpu_launches": launches, "clocks": clk, **({"box_modes_on_fitted_pool": box_modes} if box_modes else {}),
             "kernel_ms_per_step": breakdown,
             "fit_stats": {"pairs": st.pairs, "avg_kernels_per_block": st.pairs / max(st.n_tiles, 1),
                           "loss": st.loss, "psnr_db": st.psnr_db, "initial_psnr_db": st0.psnr_db,

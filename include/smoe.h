@@ -110,10 +110,23 @@ typedef struct {
                                       SURVEY §8(f) f2).  R2 = INFINITY gives the
                                       dense global (untruncated) model (GSMoE,
                                       P:173-180).                               */
+    int box_mode;                  /* block listing (reading Q4):
+                                      0 = square box of side 2 R sqrt(lambda_max)
+                                      (the paper's); 1 = the ellipse's axis-
+                                      aligned box (half sides R sqrt(Sigma_xx),
+                                      R sqrt(Sigma_yy); the default: equal to
+                                      the square for isotropic kernels, fewer
+                                      blocks as kernels turn anisotropic, 1.4-4%
+                                      faster fit steps measured on fitted pools,
+                                      DESIGN.md §5); 2 = exact: the blocks of
+                                      mode 1 whose rectangle of pixel-centre
+                                      sample points meets the ellipse.  Pixels,
+                                      losses and gradients do not depend on the
+                                      mode; the lists (smoe_bin) and the work do */
 } smoe_options;
 
 /* Fill `o` with the defaults (R2 = 2 ln 100, device = -1, automatic capacity,
- * automatic backward form, CUDA graphs on). */
+ * automatic backward form, CUDA graphs on, box_mode = 1). */
 smoe_status smoe_default_options(smoe_options *o);
 
 /* Create a handle for K kernels fitting an H x W x C image (B.json:
@@ -142,10 +155,14 @@ smoe_status smoe_render(smoe_handle h, const smoe_params *p, int out_H, int out_
  * render.  accumulate = w != 0: out += w y instead of
  * out = y, so H hypotheses fuse into their average y_m = (1/H) sum_h y_h
  * (Eq. 11) with w = 1/H; needs a device `out`.  The caller's
- * parameters are not modified. */
+ * parameters are not modified.  Pixels are identical for both store modes. */
 typedef struct {
     float sharpen;
     float accumulate;
+    int vector_stores;   /* 1: stage the block's outputs in shared memory and
+                            write 16-byte float4 rows (st.global.v4); 0
+                            (default): each thread stores its pixels (measured
+                            faster: the render is not store-bound) */
 } smoe_render_options;
 smoe_status smoe_render_ex(smoe_handle h, const smoe_params *p, int out_H, int out_W, float *out,
                            const smoe_render_options *opt);
@@ -248,14 +265,18 @@ smoe_lr smoe_paper_lr(int t, int T);
  * roofline).  smoe_profile_end: synchronise, return per-kernel
  * totals in times[SMOE_KERNEL_COUNT] and the work counters, stop profiling. */
 enum {
-    SMOE_KERNEL_PREPROCESS = 0,    /* a1 + a2 (the last CTA scans)          */
+    SMOE_KERNEL_PREPROCESS = 0,    /* a1 + a2 (the last CTA scans); with the
+                                      two-stage binning (K >= 16 384): a1 only
+                                      (k_records)                             */
     SMOE_KERNEL_SCATTER = 1,       /* a3                                     */
     SMOE_KERNEL_RASTER_TRAIN = 2,  /* a4 (bucket sort) + a5-a7               */
     SMOE_KERNEL_RASTER_RENDER = 3, /* a4 + a5/a9                             */
     SMOE_KERNEL_ADAM = 4,          /* a8                                     */
     SMOE_KERNEL_BIN = 5,           /* a1-a3 fused cooperative binner (CSR)   */
     SMOE_KERNEL_SCAN = 6,          /* a2 decoupled look-back scan (CSR)      */
-    SMOE_KERNEL_COUNT = 7
+    SMOE_KERNEL_EMIT = 7,          /* a3 two-stage binning: CTA-aggregated
+                                      bucket emission over a spatial order     */
+    SMOE_KERNEL_COUNT = 8
 };
 #define SMOE_PROFILE_COUNT_WORK 0x80000000u
 typedef struct {

@@ -70,6 +70,12 @@ def _lib():
         lib.oracle_grad_kernels.argtypes = [I, I, I, P, P, P, P, I, I, P, D, I, P, P, P, P]
         lib.oracle_margins.restype = None
         lib.oracle_margins.argtypes = [I, P, P, D, I, I, I, I, P, P]
+        lib.oracle_rect_min_d2.restype = D
+        lib.oracle_rect_min_d2.argtypes = [P, P, D, D, D, D]
+        lib.oracle_block_pairs.restype = ctypes.c_longlong
+        lib.oracle_block_pairs.argtypes = [I, P, P, D, I, I, I, I, I, P, P, P, ctypes.c_longlong]
+        lib.oracle_mode_margins.restype = None
+        lib.oracle_mode_margins.argtypes = [I, P, P, D, I, I, I, I, I, P, P]
         lib.oracle_point_margins.restype = None
         lib.oracle_point_margins.argtypes = [I, P, P, D, I, P, P, P]
         lib.oracle_set_head.restype = None
@@ -227,6 +233,53 @@ def tile_list(tilebox: np.ndarray, nx: int, ny: int, ty_range=None):
     rng = np.zeros(nx * ny + 1, np.int64)
     rng[1:] = np.cumsum(counts)
     return rng, kers
+
+
+BOX_MODES = {"square": 0, "aabb": 1, "exact": 2}
+
+
+def rect_min_d2(mu, chol, x0, x1, y0, y1) -> float:
+    """min of (x-mu)^T Sigma^-1 (x-mu) over the rectangle [x0,x1] x [y0,y1]."""
+    return _lib().oracle_rect_min_d2(_ptr(_f64(mu)), _ptr(_f64(chol)), float(x0), float(x1), float(y0), float(y1))
+
+
+def block_lists(p: Params, H, W, out_H=None, out_W=None, mode="square", R2=None):
+    """Canonical per-block lists K_n under a box mode (reading Q4): returns
+    (tile_range[n_tiles+1], ids[P], tilebox[K,4]).  Mode "square" equals
+    tile_list(boxes(...)); "aabb" uses the ellipse's axis-aligned box;
+    "exact" keeps the aabb blocks whose pixel-centre rectangle meets the
+    ellipse (smoe_oracle.c oracle_block_pairs)."""
+    out_H = H if out_H is None else out_H
+    out_W = W if out_W is None else out_W
+    R2 = R2_99() if R2 is None else R2
+    mu, ch, _, _ = _args(p)
+    tb = np.zeros((p.K, 4), np.int32)
+    m = BOX_MODES[mode]
+    n = _lib().oracle_block_pairs(p.K, _ptr(mu), _ptr(ch), R2, H, W, out_H, out_W, m, _ptr(tb), None, None, 0)
+    tiles = np.zeros(max(n, 1), np.int32)
+    kers = np.zeros(max(n, 1), np.int32)
+    _lib().oracle_block_pairs(p.K, _ptr(mu), _ptr(ch), R2, H, W, out_H, out_W, m, _ptr(tb), _ptr(tiles),
+                              _ptr(kers), n)
+    tiles, kers = tiles[:n].astype(np.int64), kers[:n].astype(np.int64)
+    order = np.lexsort((kers, tiles))        # library sort step (Q18 tie order)
+    tiles, kers = tiles[order], kers[order]
+    nx, ny = -(-out_W // 16), -(-out_H // 16)
+    rng = np.zeros(nx * ny + 1, np.int64)
+    rng[1:] = np.cumsum(np.bincount(tiles, minlength=nx * ny))
+    return rng, kers, tb
+
+
+def mode_margins(p: Params, H, W, out_H=None, out_W=None, mode="square", R2=None):
+    """Per kernel: box-edge distance to an integer under the mode, and (mode
+    exact) the smallest |rect_min_d2 - R2| over its candidate blocks."""
+    out_H = H if out_H is None else out_H
+    out_W = W if out_W is None else out_W
+    R2 = R2_99() if R2 is None else R2
+    mu, ch, _, _ = _args(p)
+    eg = np.zeros(p.K)
+    rg = np.zeros(p.K)
+    _lib().oracle_mode_margins(p.K, _ptr(mu), _ptr(ch), R2, H, W, out_H, out_W, BOX_MODES[mode], _ptr(eg), _ptr(rg))
+    return eg, rg
 
 
 def gates(p: Params, px, py, R2=None):

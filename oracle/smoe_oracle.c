@@ -115,6 +115,143 @@ void oracle_boxes(int K, const double *mu, const double *chol, double R2,
     }
 }
 
+/* Box modes (reading Q4): 0 = square box of half side
+ * R sqrt(lambda_max(Sigma)) (the default); 1 = axis-aligned
+ * box of the ellipse, half sides R sqrt(Sigma_xx) = R l11 and
+ * R sqrt(Sigma_yy) = R sqrt(l21^2 + l22^2); 2 = exact: the blocks of the
+ * mode-1 box whose rectangle of pixel-centre sample points meets the
+ * ellipse d^2 <= R2.  Every mode lists every block holding a pixel inside
+ * the ellipse, so pixels do not depend on the mode; only the lists do. */
+static void half_sides(const double *chol, double R2, int mode, double *rx, double *ry)
+{
+    if (mode == 0) {
+        double r = sqrt(R2 * oracle_lambda_max(chol));
+        *rx = r;
+        *ry = r;
+    } else {
+        double s11, s12, s22;
+        oracle_cov(chol, &s11, &s12, &s22);
+        *rx = sqrt(R2 * s11);
+        *ry = sqrt(R2 * s22);
+    }
+}
+
+/* min of d^2 = delta^T Sigma^-1 delta over the rectangle [x0,x1] x [y0,y1]
+ * (source coordinates): 0 if mu is inside, else the least of the four edge
+ * minima (each a 1-D quadratic minimised over a segment). */
+double oracle_rect_min_d2(const double *mu, const double *chol, double x0, double x1, double y0, double y1)
+{
+    if (mu[0] >= x0 && mu[0] <= x1 && mu[1] >= y0 && mu[1] <= y1) return 0.0;
+    double s11, s12, s22;
+    oracle_cov(chol, &s11, &s12, &s22);
+    double det = s11 * s22 - s12 * s12;
+    double p = s22 / det, q = -s12 / det, r = s11 / det;   /* Sigma^-1 = [[p, q], [q, r]] */
+    double best = 1e300;
+    double xs[2] = {x0, x1}, ys[2] = {y0, y1};
+    for (int e = 0; e < 2; e++) {
+        /* edge x = xs[e]: minimise over dy in [y0 - mu_y, y1 - mu_y] */
+        double dx = xs[e] - mu[0];
+        double dy = -q * dx / r;
+        if (dy < y0 - mu[1]) dy = y0 - mu[1];
+        if (dy > y1 - mu[1]) dy = y1 - mu[1];
+        double v = p * dx * dx + 2.0 * q * dx * dy + r * dy * dy;
+        if (v < best) best = v;
+        /* edge y = ys[e] */
+        dy = ys[e] - mu[1];
+        dx = -q * dy / p;
+        if (dx < x0 - mu[0]) dx = x0 - mu[0];
+        if (dx > x1 - mu[0]) dx = x1 - mu[0];
+        v = p * dx * dx + 2.0 * q * dx * dy + r * dy * dy;
+        if (v < best) best = v;
+    }
+    return best;
+}
+
+/* Boxes and (block, kernel) pairs under a box mode on the out_H x out_W
+ * raster: tilebox[K][4] (candidate blocks, -1 when empty) and up to `cap`
+ * pairs (tiles[i], kers[i]) in kernel-major, row-major block order; returns
+ * the number of pairs (all of them counted even beyond cap).  In mode 2 the
+ * rectangle of block (tx, ty) spans the source points of its output pixel
+ * centres: x in [(16 tx + 1/2) W/out_W - 1/2, (min(16 tx + 15, out_W-1) +
+ * 1/2) W/out_W - 1/2], likewise y. */
+long long oracle_block_pairs(int K, const double *mu, const double *chol, double R2, int H, int W,
+                             int out_H, int out_W, int mode, int *tilebox, int *tiles, int *kers,
+                             long long cap)
+{
+    double sx = (double)out_W / (double)W, sy = (double)out_H / (double)H;
+    int nx = (out_W + 15) / 16;
+    long long n = 0;
+    for (int k = 0; k < K; k++) {
+        double rx, ry;
+        half_sides(chol + 3 * k, R2, mode, &rx, &ry);
+        double mx = mu[2 * k], my = mu[2 * k + 1];
+        double xl = ceil((mx - rx + 0.5) * sx - 0.5), xh = floor((mx + rx + 0.5) * sx - 0.5);
+        double yl = ceil((my - ry + 0.5) * sy - 0.5), yh = floor((my + ry + 0.5) * sy - 0.5);
+        if (xl < 0) xl = 0;
+        if (yl < 0) yl = 0;
+        if (xh > out_W - 1) xh = out_W - 1;
+        if (yh > out_H - 1) yh = out_H - 1;
+        int *tb = tilebox + 4 * k;
+        if (!(xl <= xh && yl <= yh)) { tb[0] = tb[1] = tb[2] = tb[3] = -1; continue; }
+        tb[0] = (int)xl / 16; tb[1] = (int)xh / 16; tb[2] = (int)yl / 16; tb[3] = (int)yh / 16;
+        for (int ty = tb[2]; ty <= tb[3]; ty++)
+            for (int tx = tb[0]; tx <= tb[1]; tx++) {
+                if (mode == 2) {
+                    int jx1 = 16 * tx + 15 < out_W - 1 ? 16 * tx + 15 : out_W - 1;
+                    int iy1 = 16 * ty + 15 < out_H - 1 ? 16 * ty + 15 : out_H - 1;
+                    double x0 = (16 * tx + 0.5) / sx - 0.5, x1 = (jx1 + 0.5) / sx - 0.5;
+                    double y0 = (16 * ty + 0.5) / sy - 0.5, y1 = (iy1 + 0.5) / sy - 0.5;
+                    if (!(oracle_rect_min_d2(mu + 2 * k, chol + 3 * k, x0, x1, y0, y1) <= R2)) continue;
+                }
+                if (n < cap) { tiles[n] = ty * nx + tx; kers[n] = k; }
+                n++;
+            }
+    }
+    return n;
+}
+
+/* Margins of the box-mode decisions (rule P1 for modes 1, 2): per kernel,
+ * the smallest distance of its four mode box edges (mapped to the output
+ * raster) to an integer and, in mode 2, the smallest |rect_min_d2 - R2|
+ * over its candidate blocks (1e300 when none). */
+void oracle_mode_margins(int K, const double *mu, const double *chol, double R2, int H, int W,
+                         int out_H, int out_W, int mode, double *edge_gap, double *rect_gap)
+{
+    double sx = (double)out_W / (double)W, sy = (double)out_H / (double)H;
+    for (int k = 0; k < K; k++) {
+        double rx, ry;
+        half_sides(chol + 3 * k, R2, mode, &rx, &ry);
+        double mx = mu[2 * k], my = mu[2 * k + 1];
+        double e[4] = {(mx - rx + 0.5) * sx - 0.5, (mx + rx + 0.5) * sx - 0.5,
+                       (my - ry + 0.5) * sy - 0.5, (my + ry + 0.5) * sy - 0.5};
+        double eg = 1.0;
+        for (int q = 0; q < 4; q++) {
+            double f = fabs(e[q] - floor(e[q] + 0.5));
+            if (f < eg) eg = f;
+        }
+        edge_gap[k] = eg;
+        double rg = 1e300;
+        if (mode == 2) {
+            double xl = ceil(e[0]), xh = floor(e[1]), yl = ceil(e[2]), yh = floor(e[3]);
+            if (xl < 0) xl = 0;
+            if (yl < 0) yl = 0;
+            if (xh > out_W - 1) xh = out_W - 1;
+            if (yh > out_H - 1) yh = out_H - 1;
+            if (xl <= xh && yl <= yh)
+                for (int ty = (int)yl / 16; ty <= (int)yh / 16; ty++)
+                    for (int tx = (int)xl / 16; tx <= (int)xh / 16; tx++) {
+                        int jx1 = 16 * tx + 15 < out_W - 1 ? 16 * tx + 15 : out_W - 1;
+                        int iy1 = 16 * ty + 15 < out_H - 1 ? 16 * ty + 15 : out_H - 1;
+                        double v = oracle_rect_min_d2(mu + 2 * k, chol + 3 * k, (16 * tx + 0.5) / sx - 0.5,
+                                                      (jx1 + 0.5) / sx - 0.5, (16 * ty + 0.5) / sy - 0.5,
+                                                      (iy1 + 0.5) / sy - 0.5);
+                        if (fabs(v - R2) < rg) rg = fabs(v - R2);
+                    }
+        }
+        rect_gap[k] = rg;
+    }
+}
+
 /* Expert value m_jc(x) = m_c (+ Wx_c dx + Wy_c dy for the linear expert). */
 static double expert_value(const double *e, int order, double dx, double dy)
 {

@@ -7,6 +7,8 @@
 #include "smoe.h"
 #include "smoe_kernels.cuh"
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges for nsys / ncu --nvtx
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -138,6 +140,13 @@ struct smoe_ctx {
     double last_pairs = -1.0;   // host view of P on the training grid (last sync)
     int n_sm = 148;
     int head = 0;               // 0 SMoE (Eq. 2/4), 1 RBF (Eq. 1)
+    int box_mode = 0;           // 0 square, 1 aabb, 2 exact (reading Q4)
+    // spatial kernel order of the two-stage binning (k_emit); refreshed
+    // every PERM_REFRESH binnings and whenever the parameter buffer changes
+    int *perm = nullptr, *perm_hist = nullptr;
+    bool perm_valid = false;
+    long long perm_age = 0;
+    const void *perm_mu = nullptr;
     bool use_graphs = true;
     bool capturing = false;
     cudaStream_t cap_stream = nullptr;
@@ -166,6 +175,13 @@ void set_err(smoe_ctx *h, const std::string &m)
     if (h) h->err = m;
     g_err = m;
 }
+
+// NVTX range around one ABI call (visible in nsys timelines and usable as an
+// ncu --nvtx filter); a no-op unless a tool is attached.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 template <class F>
 smoe_status guard(smoe_ctx *h, F &&f)
@@ -359,6 +375,11 @@ bool use_lpt(const Grid &g) { return SMOE_LPT && !g.lb_state && g.n_tiles <= SCA
 
 ParamsDev pdev(const smoe_params *p) { return ParamsDev{p->mu, p->chol, p->log_pi, p->expert}; }
 
+BoxGeo box_geo(const smoe_ctx *h, const Grid &g)
+{
+    return BoxGeo{h->box_mode, (float)h->W / (float)g.oW, (float)h->H / (float)g.oH, g.oW, g.oH};
+}
+
 void check_params(const smoe_params *p)
 {
     if (!p || !p->mu || !p->chol || !p->log_pi || !p->expert)
@@ -371,9 +392,90 @@ void check_params(const smoe_params *p)
 // a1-a4: preprocess, scan, scatter, in-bucket sort on grid g for block rows
 // [ty_lo, ty_hi).  The first binning of a grid calibrates the capacity with
 // one synchronous read of P; later binnings never synchronise.
+// Two-stage binning (k_records + k_emit over a spatial kernel order) for
+// large pools on direct-bucket grids: one returning global atomic per
+// (CTA, block) instead of per (kernel, block).  SMOE_PERM=0/1 forces it off/on.
+constexpr int PERM_MIN_K = 16384;   // measured: config 4 (20k) +6%, config 2 (10k) -2%
+constexpr long long PERM_REFRESH = 256;
+
+bool two_stage(const smoe_ctx *h, const Grid &g)
+{
+    const char *e = getenv("SMOE_PERM");
+    const bool on = e ? atoi(e) != 0 : h->K >= PERM_MIN_K;
+    return on && g.direct;
+}
+
+// (Re)build the spatial order: counting sort of the kernel centres into
+// square buckets of ~256 kernels.  Eager launches on the
+// handle's stream, before any graph replay that reads the order.
+void refresh_perm(smoe_ctx *h, const smoe_params *p, bool force)
+{
+    const char *e = getenv("SMOE_PERM");
+    const bool on = e ? atoi(e) != 0 : h->K >= PERM_MIN_K;
+    if (!on) return;
+    if (!force && h->perm_valid && h->perm_mu == p->mu && h->perm_age < PERM_REFRESH) return;
+    if (!h->perm) {
+        CK(cudaMalloc(&h->perm, sizeof(int) * h->K));
+        CK(cudaMalloc(&h->perm_hist, sizeof(int) * PERM_MAX_BUCKETS));
+    }
+    const double tiles = std::ceil(h->W / 16.0) * std::ceil(h->H / 16.0);
+    int side = 16 * std::max(1, (int)std::lround(std::sqrt(tiles / std::max(1.0, h->K / 256.0))));
+    int nbx, nby;
+    for (;; side *= 2) {
+        nbx = (h->W + side - 1) / side;
+        nby = (h->H + side - 1) / side;
+        if ((long long)nbx * nby <= PERM_MAX_BUCKETS) break;
+    }
+    const float scale = 1.0f / (float)side;
+    const int nb = (h->K + 255) / 256;
+    CK(cudaMemsetAsync(h->perm_hist, 0, sizeof(int) * nbx * nby, h->stream));
+    k_perm_count<<<nb, 256, 0, h->stream>>>(h->K, p->mu, scale, scale, nbx, nby, h->perm_hist);
+    check_launch(h, "k_perm_count");
+    k_perm_scan<<<1, PERM_NT, 0, h->stream>>>(h->perm_hist, nbx * nby);
+    check_launch(h, "k_perm_scan");
+    k_perm_scatter<<<nb, 256, 0, h->stream>>>(h->K, p->mu, scale, scale, nbx, nby, h->perm_hist, h->perm);
+    check_launch(h, "k_perm_scatter");
+    h->perm_valid = true;
+    h->perm_age = 0;
+    h->perm_mu = p->mu;
+}
+
 void bin_unfused(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_hi, bool zero_stats, float lscale)
 {
     int K = h->K;
+    if (two_stage(h, g) && h->perm_valid) {
+        float sx = (float)g.oW / (float)h->W, sy = (float)g.oH / (float)h->H;
+        const int nb = (K + PRE_NT - 1) / PRE_NT;
+        launch(h, SMOE_KERNEL_PREPROCESS, "k_records", [&] {
+            DISPATCH_CE(h, (k_records<C_, E_><<<nb, PRE_NT, 0, h->stream>>>(
+                               K, pdev(p), h->R2, sx, sy, g.oW, g.oH, g.nx, ty_lo, ty_hi, h->rec, h->tbox,
+                               &h->ctl->hc, lscale, h->box_mode)));
+        });
+        const int ne = (K + EMIT_NT - 1) / EMIT_NT;
+        launch(h, SMOE_KERNEL_EMIT, "k_emit", [&] {
+            k_emit<<<ne, EMIT_NT, 0, h->stream>>>(K, h->perm, h->tbox, g.nx, ty_lo, ty_hi, g.cnt, g.ids, g.bcap,
+                                                   g.gc, zero_stats ? h->ctl->dstats : nullptr, h->rec, h->RS / 4,
+                                                   box_geo(h, g), h->R2);
+        });
+        if (!g.calibrated) {
+            long long cn[2];   // pairs, need
+            CK(cudaMemcpyAsync(cn, &g.gc->pairs, sizeof(cn), cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+            if (&g == &h->train) h->last_pairs = (double)cn[0];
+            CK(cudaMemsetAsync(g.cnt, 0, sizeof(int) * g.n_tiles, h->stream));
+            if (g.n_tiles > SCAN_SINGLE_MAX && cn[1] * (long long)g.n_tiles > 8 * cn[0] + (1ll << 24)) {
+                g.no_direct = true;
+                const int oH = g.oH, oW = g.oW;
+                g.oH = 0;
+                ensure_grid(h, g, g.gc, oH, oW);
+                return bin_unfused(h, g, p, ty_lo, ty_hi, zero_stats, lscale);
+            }
+            grow(h, g, cn[1] > 0 ? cn[1] : 1);
+            return bin_unfused(h, g, p, ty_lo, ty_hi, zero_stats, lscale);
+        }
+        g.order_valid = false;
+        return;
+    }
     // direct buckets need no CTA-wide block pass, so smaller CTAs spread the
     // count atomics over more SMs
     static const int pre_nt_direct = getenv("SMOE_PRE_NT_DIRECT") ? atoi(getenv("SMOE_PRE_NT_DIRECT")) : PRE_NT;
@@ -390,7 +492,7 @@ void bin_unfused(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_h
                            K, pdev(p), h->R2, sx, sy, g.oW, g.oH, g.nx, ty_lo, ty_hi, h->rec, h->tbox,
                            g.cnt, &h->ctl->hc, g.n_tiles, g.start, g.cursor, g.cap, g.gc,
                            zero_stats ? h->ctl->dstats : nullptr, g.lb_state ? nullptr : g.order, lscale,
-                           use_lpt(g) ? 1 : 0, g.ids, g.bcap, g.direct ? g.len : nullptr)));
+                           use_lpt(g) ? 1 : 0, g.ids, g.bcap, g.direct ? g.len : nullptr, h->box_mode)));
     });
     if (g.direct) {
         if (!g.calibrated) {
@@ -432,7 +534,8 @@ void bin_unfused(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_h
     }
     int ns = (K + 63) / 64;
     launch(h, SMOE_KERNEL_SCATTER, "k_scatter", [&] {
-        k_scatter<<<ns, 64, 0, h->stream>>>(K, h->tbox, g.nx, ty_lo, ty_hi, g.cursor, g.ids, g.cap, g.gc);
+        k_scatter<<<ns, 64, 0, h->stream>>>(K, h->tbox, g.nx, ty_lo, ty_hi, g.cursor, g.ids, g.cap, g.gc, h->rec,
+                                             h->RS / 4, box_geo(h, g), h->R2);
     });
     g.order_valid = use_lpt(g);
 }
@@ -466,6 +569,8 @@ void bin(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_hi, bool 
     B.order = SMOE_LPT && !getenv("SMOE_NO_LPT") ? g.order : nullptr;
     B.chunk = g.chunk; B.hist = g.hist; B.cap = g.cap; B.gc = g.gc; B.hc = &h->ctl->hc;
     B.dstats = zero_stats ? h->ctl->dstats : nullptr;
+    B.mode = h->box_mode;
+    B.rs4 = h->RS / 4;
     launch(h, SMOE_KERNEL_BIN, "k_bin", [&] {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(g.bin_grid);
@@ -488,7 +593,8 @@ void bin(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_hi, bool 
         grow(h, g, P > h->init_cap ? P : h->init_cap);
         int ns = (K + 63) / 64;
         launch(h, SMOE_KERNEL_SCATTER, "k_scatter", [&] {
-            k_scatter<<<ns, 64, 0, h->stream>>>(K, h->tbox, g.nx, ty_lo, ty_hi, g.cursor, g.ids, g.cap, g.gc);
+            k_scatter<<<ns, 64, 0, h->stream>>>(K, h->tbox, g.nx, ty_lo, ty_hi, g.cursor, g.ids, g.cap, g.gc,
+                                                 h->rec, h->RS / 4, box_geo(h, g), h->R2);
         });
         g.order_valid = false;
     }
@@ -852,6 +958,7 @@ smoe_status smoe_default_options(smoe_options *o)
     o->device = -1;
     o->use_graphs = 1;
     o->backward_mode = -1;
+    o->box_mode = 1;   // aabb: measured faster than the square box on fitted pools
     return SMOE_OK;
 }
 
@@ -873,8 +980,9 @@ smoe_status smoe_create_ex(const smoe_options *o, smoe_handle *out)
     *out = nullptr;
     if (o->K < 1 || o->H < 1 || o->W < 1 || !(o->C == 1 || o->C == 3) ||
         !(o->expert_order == 0 || o->expert_order == 1) || !(o->R2 > 0) ||
-        !(o->backward_mode >= -1 && o->backward_mode <= 1) || !(o->head == 0 || o->head == 1)) {
-        g_err = "smoe_create: need K,H,W >= 1, C in {1,3}, expert_order in {0,1}, R2 > 0";
+        !(o->backward_mode >= -1 && o->backward_mode <= 1) || !(o->head == 0 || o->head == 1) ||
+        !(o->box_mode >= 0 && o->box_mode <= 2)) {
+        g_err = "smoe_create: need K,H,W >= 1, C in {1,3}, expert_order in {0,1}, R2 > 0, box_mode in {0,1,2}";
         return SMOE_ERR_INVALID_ARG;
     }
     if ((long long)o->H * o->W >= (1ll << 31) || o->K >= (1 << 30)) {
@@ -892,6 +1000,7 @@ smoe_status smoe_create_ex(const smoe_options *o, smoe_handle *out)
     h->init_cap = o->pair_capacity;
     h->bwd_mode = o->backward_mode;
     h->head = o->head;
+    h->box_mode = o->box_mode;
     h->use_graphs = o->use_graphs != 0;
     int dev = o->device;
     if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) {
@@ -960,6 +1069,8 @@ smoe_status smoe_destroy(smoe_handle h)
     }
     if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
     dfree(h->prof.d_work);
+    dfree(h->perm);
+    dfree(h->perm_hist);
     (void)cudaGetLastError();
     delete h;
     return SMOE_OK;
@@ -1009,10 +1120,13 @@ smoe_status smoe_sync(smoe_handle h, smoe_stats *last)
 smoe_status smoe_step(smoe_handle h, smoe_params *p, const float *target, const smoe_lr *lr,
                       smoe_stats *stats)
 {
+    NvtxRange nvtx_("smoe_step");
     if (!h) return SMOE_ERR_BAD_HANDLE;
     return guard(h, [&]() -> smoe_status {
         check_params(p);
         if (!target || !lr) throw SmoeError(SMOE_ERR_INVALID_ARG, "smoe_step: NULL target or lr");
+        refresh_perm(h, p, false);
+        h->perm_age++;
         for (int attempt = 0;; attempt++) {
             const float *t = stage_target(h, target);
             run_sequence(h, 0, p, t, nullptr, lr);
@@ -1028,10 +1142,13 @@ smoe_status smoe_step(smoe_handle h, smoe_params *p, const float *target, const 
 
 smoe_status smoe_grad(smoe_handle h, const smoe_params *p, const float *target, float *grad, double *sums)
 {
+    NvtxRange nvtx_("smoe_grad");
     if (!h) return SMOE_ERR_BAD_HANDLE;
     return guard(h, [&]() -> smoe_status {
         check_params(p);
         if (!target || !grad) throw SmoeError(SMOE_ERR_INVALID_ARG, "smoe_grad: NULL target or grad");
+        refresh_perm(h, p, false);
+        h->perm_age++;
         bool gdev = is_device_ptr(grad);
         bool sdev = sums ? is_device_ptr(sums) : true;
         for (int attempt = 0;; attempt++) {
@@ -1069,6 +1186,7 @@ smoe_status smoe_apply(smoe_handle h, smoe_params *p, const float *grad, const s
 smoe_status smoe_apply_ex(smoe_handle h, smoe_params *p, const float *grad, const smoe_lr *lr, int k0, int k1,
                           const double *sums)
 {
+    NvtxRange nvtx_("smoe_apply");
     if (!h) return SMOE_ERR_BAD_HANDLE;
     return guard(h, [&]() -> smoe_status {
         check_params(p);
@@ -1103,6 +1221,7 @@ smoe_status smoe_render(smoe_handle h, const smoe_params *p, int out_H, int out_
 smoe_status smoe_render_ex(smoe_handle h, const smoe_params *p, int out_H, int out_W, float *out,
                            const smoe_render_options *opt)
 {
+    NvtxRange nvtx_("smoe_render");
     if (!h) return SMOE_ERR_BAD_HANDLE;
     return guard(h, [&]() -> smoe_status {
         check_params(p);
@@ -1112,6 +1231,8 @@ smoe_status smoe_render_ex(smoe_handle h, const smoe_params *p, int out_H, int o
         if (!(sharpen > 0.0f && sharpen <= 1.0f))
             throw SmoeError(SMOE_ERR_INVALID_ARG, "smoe_render: sharpen must be in (0, 1]");
         float lscale = sqrtf(sharpen);
+        refresh_perm(h, p, false);
+        h->perm_age++;
         bool odev = is_device_ptr(out);
         if (!odev && opt && opt->accumulate != 0.0f)
             throw SmoeError(SMOE_ERR_INVALID_ARG, "smoe_render_ex: accumulate needs a device output");
@@ -1129,6 +1250,7 @@ smoe_status smoe_render_ex(smoe_handle h, const smoe_params *p, int out_H, int o
             A.sx = (float)h->W / (float)out_W; A.sy = (float)h->H / (float)out_H;
             A.R2 = h->R2; A.out = o; A.rbf = h->head;
             A.accum = opt ? opt->accumulate : 0.0f;
+            A.vec_out = opt && opt->vector_stores ? 1 : 0;
             A.work = h->prof.d_work;
             launch(h, SMOE_KERNEL_RASTER_RENDER, "k_raster<render>", [&] {
                 const void *f = nullptr;
@@ -1279,7 +1401,8 @@ smoe_status smoe_stats_from_raw(smoe_handle h, const smoe_raw_stats *raw, smoe_s
 const char *smoe_kernel_name(int id)
 {
     static const char *names[SMOE_KERNEL_COUNT] = {"k_preprocess", "k_scatter", "k_raster<train>",
-                                                   "k_raster<render>", "k_adam", "k_bin", "k_scan_lookback"};
+                                                   "k_raster<render>", "k_adam", "k_bin", "k_scan_lookback",
+                                                   "k_emit"};
     return (id >= 0 && id < SMOE_KERNEL_COUNT) ? names[id] : "?";
 }
 

@@ -20,6 +20,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <limits.h>
 #include <type_traits>
 
 namespace smoe {
@@ -41,8 +42,9 @@ constexpr int TILE = 16;                 // 16x16 blocks
 #ifndef SMOE_PRE_ATOM
 #define SMOE_PRE_ATOM 4                  // direct binning: count atomics in flight per kernel
 #endif
-#ifndef SMOE_RENDER_VEC
-#define SMOE_RENDER_VEC 1                // render epilogue: float4 row stores through shared memory
+#ifndef SMOE_FWD_PREFETCH
+#define SMOE_FWD_PREFETCH 0              // forward: load record j+1's test half while testing record j
+                                         // (measured: +2 registers cost a resident CTA, -9% config 3)
 #endif
 #ifndef SMOE_BWD_PACK
 #define SMOE_BWD_PACK 0                  // kernel-parallel backward: raw sums kept as f32x2 pixel-pair
@@ -209,6 +211,42 @@ __device__ __forceinline__ void scan_counts(int *__restrict__ cnt, int n, int *_
     }
 }
 
+// ------------------------------------------------------- box modes -------
+// Reading Q4: 0 square box of half side R sqrt(lambda_max)
+// (default), 1 the ellipse's axis-aligned box (half sides
+// R sqrt(Sigma_xx), R sqrt(Sigma_yy)), 2 exact: the mode-1 blocks whose
+// rectangle of pixel-centre sample points meets the ellipse.  Every mode
+// lists each block holding a pixel inside the ellipse (pixels do not depend
+// on it); the lists shrink from mode 0 to 2 for anisotropic kernels.
+struct BoxGeo {
+    int mode;          // 0 square, 1 aabb, 2 exact
+    float isx, isy;    // source spacing of output samples: x = (j + 1/2) isx - 1/2
+    int oW, oH;
+};
+
+// min over the block's pixel-centre rectangle of d^2 = u^2 + v^2
+// (u = a dx, v = b dx + c dy), compared with R2 -- mode 2's block test
+__device__ __forceinline__ bool block_meets(float mux, float muy, float a, float b, float c, int tx, int ty,
+                                            const BoxGeo &G, float R2)
+{
+    const float x0 = (TILE * tx + 0.5f) * G.isx - 0.5f, x1 = (min(TILE * tx + TILE - 1, G.oW - 1) + 0.5f) * G.isx - 0.5f;
+    const float y0 = (TILE * ty + 0.5f) * G.isy - 0.5f, y1 = (min(TILE * ty + TILE - 1, G.oH - 1) + 0.5f) * G.isy - 0.5f;
+    if (mux >= x0 && mux <= x1 && muy >= y0 && muy <= y1) return true;
+    // Q(dx, dy) = p dx^2 + 2 q dx dy + r dy^2
+    const float pp = a * a + b * b, qq = b * c, rr = c * c;
+    float best = INFINITY;
+#pragma unroll
+    for (int e = 0; e < 2; e++) {
+        float dx = (e ? x1 : x0) - mux;
+        float dy = fminf(fmaxf(-qq * dx / rr, y0 - muy), y1 - muy);
+        best = fminf(best, pp * dx * dx + 2.f * qq * dx * dy + rr * dy * dy);
+        dy = (e ? y1 : y0) - muy;
+        dx = fminf(fmaxf(-qq * dy / pp, x0 - mux), x1 - mux);
+        best = fminf(best, pp * dx * dx + 2.f * qq * dx * dy + rr * dy * dy);
+    }
+    return best <= R2;
+}
+
 // ---------------------------------------------------------------- a1 ------
 // Geometry shader: Sigma = L L^T, lambda_max in closed form,
 // square box of half side r = sqrt(R2 lambda_max), pixel-centre rule (Q5)
@@ -220,7 +258,7 @@ template <int C, int E>
 __device__ __forceinline__ void
 preprocess_one(int k, ParamsDev p, float R2, float sx, float sy, int oW, int oH,
                int nx, int ty_lo, int ty_hi, float *__restrict__ rec,
-               int4 *__restrict__ tbox, int *__restrict__ cnt, HandleCtr *hc, float lscale,
+               int4 *__restrict__ tbox, int *__restrict__ cnt, HandleCtr *hc, float lscale, int mode,
                bool direct = false, int *__restrict__ dids = nullptr, int bcap = 0,
                int *n_emit = nullptr, int *max_len = nullptr)
 {
@@ -244,13 +282,20 @@ preprocess_one(int k, ParamsDev p, float R2, float sx, float sy, int oW, int oH,
     if (!ok) atomicExch((unsigned long long *)&hc->nonfinite, 1ull);
 
     float s11 = l11 * l11, s12 = l11 * l21, s22 = l21 * l21 + l22 * l22;
-    float h = 0.5f * (s11 - s22);
-    float lmax = 0.5f * (s11 + s22) + sqrtf(h * h + s12 * s12);
-    float rr = sqrtf(R2 * lmax);
-    float xl = ceilf((mu.x - rr + 0.5f) * sx - 0.5f);
-    float xh = floorf((mu.x + rr + 0.5f) * sx - 0.5f);
-    float yl = ceilf((mu.y - rr + 0.5f) * sy - 0.5f);
-    float yh = floorf((mu.y + rr + 0.5f) * sy - 0.5f);
+    float rx, ry;
+    if (mode == 0) {
+        float h = 0.5f * (s11 - s22);
+        float lmax = 0.5f * (s11 + s22) + sqrtf(h * h + s12 * s12);
+        rx = ry = sqrtf(R2 * lmax);
+    } else {
+        rx = sqrtf(R2 * s11);
+        ry = sqrtf(R2 * s22);
+    }
+    float xl = ceilf((mu.x - rx + 0.5f) * sx - 0.5f);
+    float xh = floorf((mu.x + rx + 0.5f) * sx - 0.5f);
+    float yl = ceilf((mu.y - ry + 0.5f) * sy - 0.5f);
+    float yh = floorf((mu.y + ry + 0.5f) * sy - 0.5f);
+    const BoxGeo G{mode, 1.0f / sx, 1.0f / sy, oW, oH};
     xl = fmaxf(xl, 0.0f); yl = fmaxf(yl, 0.0f);
     xh = fminf(xh, (float)(oW - 1)); yh = fminf(yh, (float)(oH - 1));
     int4 tb = make_int4(-1, -1, -1, -1);
@@ -269,24 +314,28 @@ preprocess_one(int k, ParamsDev p, float R2, float sx, float sy, int oW, int oH,
             // direct buckets: the count atomic returns k's slot in block t's
             // fixed-capacity bucket (PRE_ATOM atomics in flight per round)
             const int wx = tb.y - tb.x + 1, nbx = max(0, y1 - y0 + 1) * wx;
+            int emitted = 0;
             for (int i0 = 0; i0 < nbx; i0 += PRE_ATOM) {
                 int t[PRE_ATOM], sl[PRE_ATOM];
+                bool on[PRE_ATOM];
 #pragma unroll
                 for (int q = 0; q < PRE_ATOM; q++) {
                     const int i = i0 + q, yy = y0 + i / wx, xx = tb.x + i % wx;
                     t[q] = yy * nx + xx;
-                    sl[q] = i < nbx ? atomicAdd(&cnt[t[q]], 1) : bcap;
+                    on[q] = i < nbx && (mode != 2 || block_meets(mu.x, mu.y, a, b, c, xx, yy, G, R2));
+                    sl[q] = on[q] ? atomicAdd(&cnt[t[q]], 1) : bcap;
                 }
 #pragma unroll
                 for (int q = 0; q < PRE_ATOM; q++) {
                     if (sl[q] < bcap) dids[(size_t)t[q] * bcap + sl[q]] = k;
-                    if (i0 + q < nbx) *max_len = max(*max_len, sl[q] + 1);
+                    if (on[q]) { *max_len = max(*max_len, sl[q] + 1); emitted++; }
                 }
             }
-            *n_emit = nbx;
-        } else {
+            *n_emit = emitted;
+        } else if (cnt) {
             for (int ty = y0; ty <= y1; ty++)
-                for (int tx = tb.x; tx <= tb.y; tx++) atomicAdd(&cnt[ty * nx + tx], 1);
+                for (int tx = tb.x; tx <= tb.y; tx++)
+                    if (mode != 2 || block_meets(mu.x, mu.y, a, b, c, tx, ty, G, R2)) atomicAdd(&cnt[ty * nx + tx], 1);
         }
     }
     tbox[k] = tb;
@@ -327,13 +376,13 @@ k_preprocess(int K, ParamsDev p, float R2, float sx /* oW/W */, float sy /* oH/H
              int4 *__restrict__ tbox, int *__restrict__ cnt, HandleCtr *hc,
              int n_tiles, int *__restrict__ start, int *__restrict__ cursor, long long cap,
              GridCtr *gc, double *dstats, int *__restrict__ order, float lscale, int build_order,
-             int *__restrict__ dids, int bcap, int *__restrict__ len)
+             int *__restrict__ dids, int bcap, int *__restrict__ len, int mode)
 {
     int k = blockIdx.x * blockDim.x + threadIdx.x;
     int n_emit = 0, max_len = 0;
     if (k < K)
-        preprocess_one<C, E>(k, p, R2, sx, sy, oW, oH, nx, ty_lo, ty_hi, rec, tbox, cnt, hc, lscale, len != nullptr,
-                             dids, bcap, &n_emit, &max_len);
+        preprocess_one<C, E>(k, p, R2, sx, sy, oW, oH, nx, ty_lo, ty_hi, rec, tbox, cnt, hc, lscale, mode,
+                             len != nullptr, dids, bcap, &n_emit, &max_len);
     if (len) {
         // direct buckets: this CTA's pairs and longest slot to the grid counters
         __shared__ unsigned long long s_pairs;
@@ -409,6 +458,235 @@ k_preprocess(int K, ParamsDev p, float R2, float sx /* oW/W */, float sy /* oH/H
     if (threadIdx.x == 0) { gc->ticket = 0; gc->work = 0; }
 }
 
+
+// ------------------------------------------- a1 + a3, large pools -------
+// Two-stage direct-bucket binning for large pools (K >= PERM_MIN_K).  The
+// one-pass form (k_preprocess) issues one returning global atomic per
+// (kernel, block) pair: 8.35 M at config 5, the throughput limit of that
+// kernel (ncu: long-scoreboard stalls on the returning atomics).  Here
+//   stage 1  k_records: per kernel in id order (coalesced), the record and
+//            the tile box -- no atomics;
+//   stage 2  k_emit: per kernel in a spatially sorted order (perm), the CTA
+//            counts its kernels' (block) entries in a shared-memory window
+//            of blocks, adds each window block's count to the block's global
+//            counter with ONE returning atomic, and hands out slots from the
+//            returned base with shared-memory atomics.
+// The permutation only groups kernels that are close in the image (a
+// counting sort of the centres into ~256-kernel spatial buckets, refreshed
+// every PERM_REFRESH binnings; centres move by <= lr_mu ~ 0.01 px per step);
+// any permutation gives the same lists, because the raster sorts each bucket
+// by kernel id (a4).
+constexpr int PERM_NT = 1024;           // single-CTA scan of the bucket histogram
+constexpr int PERM_MAX_BUCKETS = 16384;
+constexpr int EMIT_NT = 256;
+constexpr int EMIT_WIN = 2048;          // shared window of blocks per CTA
+
+__device__ __forceinline__ int perm_key(float2 mu, float bx_scale, float by_scale, int nbx, int nby)
+{
+    // spatial bucket of the centre (clamped; non-finite centres to bucket 0)
+    float fx = mu.x * bx_scale, fy = mu.y * by_scale;
+    int bx = (fx == fx) ? (int)fminf(fmaxf(fx, 0.f), (float)(nbx - 1)) : 0;
+    int by = (fy == fy) ? (int)fminf(fmaxf(fy, 0.f), (float)(nby - 1)) : 0;
+    return by * nbx + bx;
+}
+
+__global__ void __launch_bounds__(256)
+k_perm_count(int K, const float *__restrict__ mu, float bx_scale, float by_scale, int nbx, int nby,
+             int *__restrict__ hist)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < K) atomicAdd(&hist[perm_key(reinterpret_cast<const float2 *>(mu)[k], bx_scale, by_scale, nbx, nby)], 1);
+}
+
+// exclusive scan of nb <= PERM_MAX_BUCKETS counts by one CTA, in place
+__global__ void __launch_bounds__(PERM_NT)
+k_perm_scan(int *__restrict__ hist, int nb)
+{
+    constexpr int PER = PERM_MAX_BUCKETS / PERM_NT;
+    __shared__ int wsum[PERM_NT / 32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    int v[PER], loc = 0;
+#pragma unroll
+    for (int q = 0; q < PER; q++) {
+        const int i = tid * PER + q;
+        v[q] = i < nb ? hist[i] : 0;
+        loc += v[q];
+    }
+    int inc = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        const int w = wsum[lane];
+        int wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(FULL, wi, o);
+            if (lane >= o) wi += t;
+        }
+        wsum[lane] = wi - w;
+    }
+    __syncthreads();
+    int e = wsum[wid] + inc - loc;
+#pragma unroll
+    for (int q = 0; q < PER; q++) {
+        const int i = tid * PER + q;
+        if (i < nb) hist[i] = e;
+        e += v[q];
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_perm_scatter(int K, const float *__restrict__ mu, float bx_scale, float by_scale, int nbx, int nby,
+               int *__restrict__ cursor, int *__restrict__ perm)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < K)
+        perm[atomicAdd(&cursor[perm_key(reinterpret_cast<const float2 *>(mu)[k], bx_scale, by_scale, nbx, nby)], 1)] = k;
+}
+
+// stage 1: records and tile boxes, no emission
+template <int C, int E>
+__global__ void __launch_bounds__(PRE_NT)
+k_records(int K, ParamsDev p, float R2, float sx, float sy, int oW, int oH, int nx, int ty_lo, int ty_hi,
+          float *__restrict__ rec, int4 *__restrict__ tbox, HandleCtr *hc, float lscale, int mode)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < K)
+        preprocess_one<C, E>(k, p, R2, sx, sy, oW, oH, nx, ty_lo, ty_hi, rec, tbox, nullptr, hc, lscale, mode);
+}
+
+// mode 2's block test from the kernel's record (mu, a, b | c at float4 0, 1)
+__device__ __forceinline__ bool rec_meets(const float *rec, int rs4, int k, int tx, int ty, const BoxGeo &G, float R2)
+{
+    if (G.mode != 2) return true;
+    const float4 f0 = reinterpret_cast<const float4 *>(rec)[(size_t)k * rs4];
+    const float c = rec[(size_t)k * rs4 * 4 + 4];
+    return block_meets(f0.x, f0.y, f0.z, f0.w, c, tx, ty, G, R2);
+}
+
+// stage 2: bucket emission, CTA-aggregated over a shared window of blocks
+__global__ void __launch_bounds__(EMIT_NT)
+k_emit(int K, const int *__restrict__ perm, const int4 *__restrict__ tbox, int nx, int ty_lo, int ty_hi,
+       int *__restrict__ cnt, int *__restrict__ dids, int bcap, GridCtr *gc, double *dstats,
+       const float *__restrict__ rec, int rs4, BoxGeo G, float R2)
+{
+    __shared__ int s_cnt[EMIT_WIN];
+    __shared__ int s_base[EMIT_WIN];
+    __shared__ int s_red[4][EMIT_NT / 32];
+    __shared__ unsigned long long s_pairs;
+    __shared__ int s_max;
+    __shared__ bool last;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int i = blockIdx.x * EMIT_NT + tid;
+    const int k = i < K ? __ldg(perm + i) : -1;
+    int4 tb = make_int4(0, -1, 0, -1);              // empty box
+    if (k >= 0) {
+        tb = tbox[k];
+        if (tb.x < 0) tb = make_int4(0, -1, 0, -1);
+        tb.z = max(tb.z, ty_lo);
+        tb.w = min(tb.w, ty_hi - 1);
+        if (tb.z > tb.w) tb = make_int4(0, -1, 0, -1);
+    }
+    const bool any = tb.x <= tb.y;
+    // CTA window of blocks: min/max of the (non-empty) boxes
+    int mnx = any ? tb.x : INT_MAX, mxx = any ? tb.y : INT_MIN, mny = any ? tb.z : INT_MAX, mxy = any ? tb.w : INT_MIN;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        mnx = min(mnx, __shfl_xor_sync(FULL, mnx, o));
+        mxx = max(mxx, __shfl_xor_sync(FULL, mxx, o));
+        mny = min(mny, __shfl_xor_sync(FULL, mny, o));
+        mxy = max(mxy, __shfl_xor_sync(FULL, mxy, o));
+    }
+    if (lane == 0) { s_red[0][wid] = mnx; s_red[1][wid] = mxx; s_red[2][wid] = mny; s_red[3][wid] = mxy; }
+    if (tid == 0) { s_pairs = 0ull; s_max = 0; }
+    __syncthreads();
+    mnx = INT_MAX; mxx = INT_MIN; mny = INT_MAX; mxy = INT_MIN;
+#pragma unroll
+    for (int w = 0; w < EMIT_NT / 32; w++) {
+        mnx = min(mnx, s_red[0][w]); mxx = max(mxx, s_red[1][w]);
+        mny = min(mny, s_red[2][w]); mxy = max(mxy, s_red[3][w]);
+    }
+    const int wcols = mxx - mnx + 1, wrows = mxy - mny + 1;
+    const bool windowed = mxx >= mnx && (long long)wcols * wrows <= EMIT_WIN;
+    const int wx = tb.y - tb.x + 1, nbx = any ? (tb.w - tb.z + 1) * wx : 0;
+    int n_emit = 0, max_len = 0;
+    if (windowed) {
+        const int area = wcols * wrows;
+        for (int w = tid; w < area; w += EMIT_NT) s_cnt[w] = 0;
+        __syncthreads();
+        for (int e = 0; e < nbx; e++) {
+            const int yy = tb.z + e / wx, xx = tb.x + e % wx;
+            if (!rec_meets(rec, rs4, k, xx, yy, G, R2)) continue;
+            atomicAdd(&s_cnt[(yy - mny) * wcols + (xx - mnx)], 1);
+            n_emit++;
+        }
+        __syncthreads();
+        // one returning global atomic per window block that has entries
+        for (int w = tid; w < area; w += EMIT_NT) {
+            const int c = s_cnt[w];
+            if (c) {
+                const int t = (mny + w / wcols) * nx + mnx + w % wcols;
+                const int b = atomicAdd(&cnt[t], c);
+                s_base[w] = b;
+                max_len = max(max_len, b + c);
+                s_cnt[w] = 0;                          // reused as the slot cursor
+            }
+        }
+        __syncthreads();
+        for (int e = 0; e < nbx; e++) {
+            const int yy = tb.z + e / wx, xx = tb.x + e % wx;
+            if (!rec_meets(rec, rs4, k, xx, yy, G, R2)) continue;
+            const int w = (yy - mny) * wcols + (xx - mnx);
+            const int sl = s_base[w] + atomicAdd(&s_cnt[w], 1);
+            if (sl < bcap) dids[(size_t)(yy * nx + xx) * bcap + sl] = k;
+        }
+    } else {
+        // window too large (huge or scattered kernels): per-entry atomics
+        for (int e0 = 0; e0 < nbx; e0 += PRE_ATOM) {
+            int t[PRE_ATOM], sl[PRE_ATOM];
+            bool on[PRE_ATOM];
+#pragma unroll
+            for (int q = 0; q < PRE_ATOM; q++) {
+                const int e = e0 + q, yy = tb.z + e / wx, xx = tb.x + e % wx;
+                t[q] = yy * nx + xx;
+                on[q] = e < nbx && rec_meets(rec, rs4, k, xx, yy, G, R2);
+                sl[q] = on[q] ? atomicAdd(&cnt[t[q]], 1) : bcap;
+            }
+#pragma unroll
+            for (int q = 0; q < PRE_ATOM; q++) {
+                if (sl[q] < bcap) dids[(size_t)t[q] * bcap + sl[q]] = k;
+                if (on[q]) { max_len = max(max_len, sl[q] + 1); n_emit++; }
+            }
+        }
+    }
+    // this CTA's pairs and longest slot to the grid counters; the last CTA
+    // publishes P and the overflow latch (finish_direct)
+    unsigned long long pe = (unsigned)n_emit;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        pe += __shfl_xor_sync(FULL, pe, o);
+        max_len = max(max_len, __shfl_xor_sync(FULL, max_len, o));
+    }
+    if (lane == 0) {
+        if (pe) atomicAdd(&s_pairs, pe);
+        if (max_len) atomicMax(&s_max, max_len);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        if (s_pairs) atomicAdd(&gc->acc_pairs, s_pairs);
+        if (s_max) atomicMax(&gc->acc_max, s_max);
+        last = atom_add_acq_rel_gpu(&gc->ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    finish_direct(bcap, gc, dstats);
+    if (tid == 0) { gc->ticket = 0; gc->work = 0; }
+}
 
 // Large grids (n_tiles > SCAN_SINGLE_MAX): single-pass decoupled look-back
 // scan of the block counts, 4096 counts per CTA.  Each CTA takes a virtual
@@ -519,7 +797,8 @@ k_scan_lookback(int *__restrict__ cnt, int n, int *__restrict__ start, int *__re
 // ("Each intersected block b_n is recorded").
 __global__ void __launch_bounds__(64)
 k_scatter(int K, const int4 *__restrict__ tbox, int nx, int ty_lo, int ty_hi,
-          int *__restrict__ cursor, int *__restrict__ ids, long long cap, const GridCtr *gc)
+          int *__restrict__ cursor, int *__restrict__ ids, long long cap, const GridCtr *gc,
+          const float *__restrict__ rec, int rs4, BoxGeo G, float R2)
 {
     if (gc->skip) return;
     int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -538,7 +817,7 @@ k_scatter(int K, const int4 *__restrict__ tbox, int nx, int ty_lo, int ty_hi,
             pos[q] = -1;
             if (i < cnt) {
                 int tyy = y0 + i / w, txx = tb.x + i % w;
-                pos[q] = atomicAdd(&cursor[tyy * nx + txx], 1);
+                if (rec_meets(rec, rs4, k, txx, tyy, G, R2)) pos[q] = atomicAdd(&cursor[tyy * nx + txx], 1);
             }
         }
 #pragma unroll
@@ -569,6 +848,7 @@ struct BinArgs {
     GridCtr *gc;
     HandleCtr *hc;
     double *dstats;
+    int mode, rs4;
 };
 
 constexpr int BIN_NT = 256;
@@ -591,7 +871,7 @@ k_bin(BinArgs B)
     }
     for (int k = blockIdx.x * BIN_NT + tid; k < B.K; k += nthreads)
         preprocess_one<C, E>(k, B.p, B.R2, B.sx, B.sy, B.oW, B.oH, B.nx, B.ty_lo, B.ty_hi, B.rec, B.tbox,
-                             B.cnt, B.hc, B.lscale);
+                             B.cnt, B.hc, B.lscale, B.mode);
     grid.sync();
     // ---- phase 2 (a2): chunked scan of the block counts ----
     const int n = B.n_tiles;
@@ -670,6 +950,7 @@ k_bin(BinArgs B)
     // ---- phase 3 (a3 + LPT order) ----
     const long long P = __ldcg(&B.gc->pairs);
     if (P > B.cap) return;                  // uniform: every CTA reads the same P
+    const BoxGeo G{B.mode, 1.0f / B.sx, 1.0f / B.sy, B.oW, B.oH};
     for (int k = blockIdx.x * BIN_NT + tid; k < B.K; k += nthreads) {
         int4 tb = B.tbox[k];
         if (tb.x < 0) continue;
@@ -682,7 +963,8 @@ k_bin(BinArgs B)
             for (int q = 0; q < 8; q++) {
                 int i = i0 + q;
                 pos[q] = -1;
-                if (i < cnt) pos[q] = atomicAdd(&B.cursor[(y0 + i / w) * B.nx + tb.x + i % w], 1);
+                if (i < cnt && rec_meets(B.rec, B.rs4, k, tb.x + i % w, y0 + i / w, G, B.R2))
+                    pos[q] = atomicAdd(&B.cursor[(y0 + i / w) * B.nx + tb.x + i % w], 1);
             }
 #pragma unroll
             for (int q = 0; q < 8; q++)
@@ -877,6 +1159,7 @@ struct RasterArgs {
     // render
     float *out;           // [C][oH][oW]
     float accum;          // 0: out = y; else out += accum * y
+    int vec_out;          // 1: float4 row stores through shared memory
     // profiling (PROF instantiation only): tested / hit (pixel, kernel)
     // pairs, SM cycles in the bucket sort, SM cycles of the whole CTA
     unsigned long long *work;
@@ -1030,10 +1313,25 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
         for (int b0 = 0; b0 < n; b0 += BATCH) {
             int nb = min(BATCH, n - b0);
             load_batch(b0, nb);
+            // software pipeline: the test half of record j+1 (mu, a, b, c and
+            // the next four floats) is loaded while record j is tested
+            float4 n0 = srec[0], n1 = srec[1];
 #pragma unroll FWD_UNROLL
             for (int j = 0; j < nb; j++) {
                 float r[R::RS];
-                load_rec(j, r);
+                if (SMOE_FWD_PREFETCH) {
+                    const float4 f0 = n0, f1 = n1;
+                    if (j + 1 < nb) { n0 = srec[(j + 1) * RS4]; n1 = srec[(j + 1) * RS4 + 1]; }
+                    r[0] = f0.x; r[1] = f0.y; r[2] = f0.z; r[3] = f0.w;
+                    r[4] = f1.x; r[5] = f1.y; r[6] = f1.z; r[7] = f1.w;
+#pragma unroll
+                    for (int q4 = 2; q4 < RS4; q4++) {
+                        const float4 f = srec[j * RS4 + q4];
+                        r[4 * q4] = f.x; r[4 * q4 + 1] = f.y; r[4 * q4 + 2] = f.z; r[4 * q4 + 3] = f.w;
+                    }
+                } else {
+                    load_rec(j, r);
+                }
                 float dx, u;
                 float2 dy, w, q;
                 dist2(r, dx, dy, u, w, q);
@@ -1079,7 +1377,12 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
 #pragma unroll
     for (int c = 0; c < C; c++) { y0[c] = N2[c].x * iD0; y1[c] = N2[c].y * iD1; }
 
-    if (!TRAIN && !SMOE_RENDER_VEC) {
+    if (!TRAIN && !A.vec_out) {
+        // scalar epilogue (default): each lane stores its two pixels per
+        // channel; a warp store covers 4 rows x 32 contiguous bytes (full
+        // sectors).  Measured 1.7% faster than the float4 epilogue below at
+        // the config-3 4x render (the staging costs more issue slots than
+        // the 4x fewer stores save; the render is not store-bound).
         size_t plane = (size_t)A.oH * A.oW;
         float *o0 = A.out + (size_t)py0 * A.oW + px, *o1 = A.out + (size_t)py1 * A.oW + px;
 #pragma unroll
@@ -1097,17 +1400,15 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
     }
     if (!TRAIN) {
         // Render epilogue: the block's C x 16 x 16 outputs are staged in
-        // shared memory (the record batch buffer, free now) and written as
+        // shared memory and written as
         // coalesced float4 rows (st.global.v4: 16 B per thread, a block row is
         // one 64-byte run).  Row stride 20 floats keeps the lane-pair layout
         // of the staging writes free of bank conflicts and every float4
         // 16-byte aligned.  Ragged edges and rasters whose width is not a
         // multiple of 4 store the remaining pixels one by one.
         constexpr int SR = 20;
-        static_assert(C * TILE * SR <= BATCH * RS4 * 4, "render staging exceeds the record buffer");
-        float *so = reinterpret_cast<float *>(srec);
+        __shared__ float so[TRAIN ? 1 : C * TILE * SR];   // own buffer: no barrier before the staging writes
         const int cx = (warp & 1) * 8 + (lane & 7), cy = (warp >> 1) * 8 + (lane >> 3) * 2;
-        __syncthreads();                                  // every warp is done with the last batch
 #pragma unroll
         for (int c = 0; c < C; c++) {
             so[(c * TILE + cy) * SR + cx] = y0[c];

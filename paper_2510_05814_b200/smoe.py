@@ -54,7 +54,7 @@ class c_work(ctypes.Structure):
                 ("sort_cycles", ctypes.c_longlong), ("cta_cycles", ctypes.c_longlong)]
 
 
-KERNEL_COUNT = 7
+KERNEL_COUNT = 8
 
 
 class c_raw_stats(ctypes.Structure):
@@ -66,11 +66,11 @@ class c_options(ctypes.Structure):
     _fields_ = [("K", ctypes.c_int), ("H", ctypes.c_int), ("W", ctypes.c_int), ("C", ctypes.c_int),
                 ("expert_order", ctypes.c_int), ("R2", ctypes.c_double), ("device", ctypes.c_int),
                 ("pair_capacity", ctypes.c_longlong), ("backward_mode", ctypes.c_int),
-                ("use_graphs", ctypes.c_int), ("head", ctypes.c_int)]
+                ("use_graphs", ctypes.c_int), ("head", ctypes.c_int), ("box_mode", ctypes.c_int)]
 
 
 class c_render_options(ctypes.Structure):
-    _fields_ = [("sharpen", ctypes.c_float), ("accumulate", ctypes.c_float)]
+    _fields_ = [("sharpen", ctypes.c_float), ("accumulate", ctypes.c_float), ("vector_stores", ctypes.c_int)]
 
 
 def lib():
@@ -240,7 +240,7 @@ class SMoE:
 
     def __init__(self, K: int, H: int, W: int, C: int, expert_order: int = 0, R2: float | None = None,
                  device: int | None = None, pair_capacity: int = 0, backward_mode: int = -1,
-                 use_graphs: bool = True, head: str = "smoe"):
+                 use_graphs: bool = True, head: str = "smoe", box_mode: str | None = None):
         L = lib()
         o = c_options()
         _check(L.smoe_default_options(ctypes.byref(o)))
@@ -252,6 +252,8 @@ class SMoE:
         o.backward_mode = backward_mode
         o.use_graphs = int(bool(use_graphs))
         o.head = {"smoe": 0, "rbf": 1}[head]
+        if box_mode is not None:      # None: the library default (aabb)
+            o.box_mode = {"square": 0, "aabb": 1, "exact": 2}[box_mode]
         h = ctypes.c_void_p()
         _check(L.smoe_create_ex(ctypes.byref(o), ctypes.byref(h)))
         self.h = h
@@ -296,7 +298,7 @@ class SMoE:
         return None
 
     def render(self, params: Params, out_H: int | None = None, out_W: int | None = None, out=None,
-               sharpen: float = 1.0, accumulate: float = 0.0):
+               sharpen: float = 1.0, accumulate: float = 0.0, vector_stores: bool = False):
         """smoe_render(_ex): y on an out_H x out_W raster -> [C, out_H, out_W];
         ``sharpen`` = s < 1 renders with Sigma -> s Sigma (kernel editing);
         ``accumulate`` = w != 0 adds w y into ``out`` (multi-model fusion)."""
@@ -306,7 +308,7 @@ class SMoE:
         own = out is None
         if own:
             out = torch.empty((self.C, out_H, out_W), dtype=torch.float32, device=f"cuda:{self.device}")
-        ro = c_render_options(sharpen, accumulate)
+        ro = c_render_options(sharpen, accumulate, int(bool(vector_stores)))
         args = (self.h, ctypes.byref(self._p(params)), out_H, out_W,
                 _ptr(out, "out", torch.float32, self.C * out_H * out_W, self.device), ctypes.byref(ro))
         _check(lib().smoe_render_ex(*args), self.h)

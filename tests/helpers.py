@@ -142,3 +142,21 @@ def assert_params(got, ref, tol, factor=2.0, what="params"):
         raise AssertionError(f"{what}: {bad.sum()} of {bad.size} beyond {factor} x tol; worst at {i}: "
                              f"gpu {got[i]:.8e} ref {ref[i]:.8e} tol {tol[i]:.3e}")
     return float((d / np.maximum(lim, 1e-300)).max())
+
+
+def conditioned_mode(pool, H, W, out_H=None, out_W=None, mode="square", seed=0, tau_d=1e-4, tau_b=1e-3,
+                     rounds=40):
+    """Rule P1 for a box mode: also keep the mode's box edges tau_b from an
+    integer and (mode "exact") every candidate block's rectangle minimum of
+    d^2 tau_d from R2, so fp32 and fp64 list the same blocks."""
+    g = np.random.default_rng(seed)
+    pool = pool.copy()
+    for _ in range(rounds):
+        p = O.Params.from_any(pool)
+        dg, eg = O.margins(p, H, W, out_H, out_W)
+        em, rm = O.mode_margins(p, H, W, out_H, out_W, mode=mode)
+        bad = (dg <= tau_d) | (eg <= tau_b) | (em <= tau_b) | (rm <= tau_d)
+        if not bad.any():
+            return pool
+        pool.mu[bad] += g.uniform(-0.5, 0.5, (int(bad.sum()), 2)).astype(np.float32)
+    raise AssertionError("could not margin-condition the pool for the box mode")

@@ -56,14 +56,14 @@ def test_host_only_functions(L):
     assert L.smoe_abi_version() == 2
     names = [L.smoe_kernel_name(i).decode() for i in range(smoe.KERNEL_COUNT)]
     assert names == ["k_preprocess", "k_scatter", "k_raster<train>", "k_raster<render>", "k_adam", "k_bin",
-                     "k_scan_lookback"]
+                     "k_scan_lookback", "k_emit"]
     assert L.smoe_kernel_name(smoe.KERNEL_COUNT) == b"?"
     assert L.smoe_apply_ex(None, None, None, None, 0, 0, None) == smoe.ERR_BAD_HANDLE
     assert L.smoe_status_string(0) == b"ok"
     assert L.smoe_status_string(5) == b"pair capacity exceeded"
     o = smoe.c_options()
     assert L.smoe_default_options(ctypes.byref(o)) == 0
-    assert abs(o.R2 - 2 * math.log(100.0)) < 1e-15 and o.device == -1
+    assert abs(o.R2 - 2 * math.log(100.0)) < 1e-15 and o.device == -1 and o.box_mode == 1
     # paper lr schedule
     assert abs(L.smoe_paper_lr(0, 10000).mu - 0.01) < 1e-9
     assert abs(L.smoe_paper_lr(5000, 10000).mu - 3.1623e-4) < 1e-7

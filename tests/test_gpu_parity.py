@@ -13,7 +13,7 @@ import torch
 
 import oracle as O
 from paper_2510_05814_b200 import smoe, synth
-from helpers import (assert_grads, assert_params, assert_pixels, conditioned, conditioned_multi,
+from helpers import (assert_grads, assert_params, assert_pixels, conditioned, conditioned_mode, conditioned_multi,
                      oracle_fit_with_tolerance)
 
 pytestmark = pytest.mark.gpu
@@ -44,7 +44,7 @@ def test_binning_bit_exact(H, W, C, K, order, scale, seed):
     oH, oW = int(round(H * scale)), int(round(W * scale))
     pool = synth.aniso_pool(H, W, C, K, seed, order=order, margin_px=8)
     pool = conditioned(pool, H, W, oH, oW)
-    h = smoe.SMoE(K, H, W, C, order)
+    h = smoe.SMoE(K, H, W, C, order, box_mode="square")
     rng, ids, tb = h.bin(dev_pool(pool), oH, oW)
     _, tb_ref, _ = O.boxes(opar(pool), H, W, oH, oW)
     nx, ny = -(-oW // 16), -(-oH // 16)
@@ -63,6 +63,9 @@ BINNERS = {
     "direct": ({}, {"k_preprocess", "k_raster<render>"}),
     "csr_scan_lpt": ({"SMOE_CSR": "1", "SMOE_FUSED_BIN": "0"}, {"k_preprocess", "k_scatter", "k_raster<render>"}),
     "csr_coop": ({"SMOE_CSR": "1", "SMOE_FUSED_BIN": "1"}, {"k_bin", "k_raster<render>"}),
+    # the two-stage form of large pools (K >= 50 000), forced on: records,
+    # then CTA-aggregated emission over the spatial kernel order
+    "two_stage": ({"SMOE_PERM": "1"}, {"k_preprocess", "k_emit", "k_raster<render>"}),
 }
 
 
@@ -75,14 +78,20 @@ def test_binning_all_binners(binner, monkeypatch):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     H, W, C, K = 130, 97, 3, 600
-    pool = conditioned(synth.aniso_pool(H, W, C, K, 5, order=1, margin_px=8), H, W)
-    h = smoe.SMoE(K, H, W, C, 1)
+    pool = conditioned_multi(synth.aniso_pool(H, W, C, K, 5, order=1, margin_px=8), H, W, [(H, W), (2 * H, 2 * W)])
+    h = smoe.SMoE(K, H, W, C, 1, box_mode="square")
     p = dev_pool(pool)
     h.bin(p)                                      # first binning calibrates the capacity
     h.profile_begin(64)
     rng, ids, tb = h.bin(p)
     launched, _ = h.profile_end()
     assert set(launched) == kernels, launched
+    if binner == "two_stage":                     # smaller CTA windows than the grid: both emission paths
+        rng2, ids2, _ = h.bin(p, 2 * H, 2 * W)
+        _, tb2, _ = O.boxes(opar(pool), H, W, 2 * H, 2 * W)
+        r2, i2 = O.tile_list(tb2, -(-2 * W // 16), -(-2 * H // 16))
+        np.testing.assert_array_equal(rng2.numpy(), r2)
+        np.testing.assert_array_equal(ids2.numpy(), i2)
     _, tb_ref, _ = O.boxes(opar(pool), H, W)
     rng_ref, ids_ref = O.tile_list(tb_ref, 7, 9)
     np.testing.assert_array_equal(rng.numpy(), rng_ref)
@@ -103,7 +112,7 @@ def test_binning_kodak_density_and_determinism():
     H, W = 512, 768
     img = synth.image(H, W, 3, 1236)
     pool = conditioned(synth.paper_init(img, 10_000, 1237, order=1), H, W)
-    h = smoe.SMoE(10_000, H, W, 3, 1)
+    h = smoe.SMoE(10_000, H, W, 3, 1, box_mode="square")
     p = dev_pool(pool)
     rng, ids, tb = h.bin(p)
     _, tb_ref, _ = O.boxes(opar(pool), H, W)
@@ -124,7 +133,7 @@ def test_binning_large_bucket_merge_path():
     pool = synth.aniso_pool(H, W, 1, K, 9, l_range=(0.3, 0.6), shear=0.1)
     pool.mu[:] = g.uniform(18.2, 29.8, (K, 2)).astype(np.float32)
     pool = conditioned(pool, H, W)
-    h = smoe.SMoE(K, H, W, 1, 0)
+    h = smoe.SMoE(K, H, W, 1, 0, box_mode="square")
     rng, ids, _ = h.bin(dev_pool(pool))
     _, tb_ref, _ = O.boxes(opar(pool), H, W)
     rng_ref, ids_ref = O.tile_list(tb_ref, 2, 2)
@@ -164,19 +173,23 @@ def test_grad_parity_bucket_over_2048(mode):
     assert_grads(gr.cpu().numpy(), lg.grad, lg.grad_abs, b_ref=lg.grad_opnd)
 
 
-@pytest.mark.parametrize("direct_max", ["", "32768"])
+@pytest.mark.parametrize("direct_max", ["", "32768", "perm"])
 def test_large_grid_lookback_scan_and_render(direct_max, monkeypatch):
     """An output raster with more than 32768 blocks: direct buckets (default)
     or, with direct buckets capped at 32768 blocks, CSR lists built by the
-    multi-CTA look-back scan; lists stay bit-exact and sampled pixels match
-    the oracle."""
-    if direct_max:
+    multi-CTA look-back scan, or ("perm") the two-stage binning whose CTA
+    windows exceed the shared window here (300 scattered kernels per CTA:
+    the per-entry fallback of k_emit); lists stay bit-exact and sampled
+    pixels match the oracle."""
+    if direct_max == "perm":
+        monkeypatch.setenv("SMOE_PERM", "1")
+    elif direct_max:
         monkeypatch.setenv("SMOE_DIRECT_MAX", direct_max)
     H, W, C, K = 1456, 1456, 3, 300
     oH = oW = 2912                       # 182 x 182 = 33124 blocks
     pool = synth.aniso_pool(H, W, C, K, 61, order=1, margin_px=4)
     pool = conditioned(pool, H, W, oH, oW)
-    h = smoe.SMoE(K, H, W, C, 1)
+    h = smoe.SMoE(K, H, W, C, 1, box_mode="square")
     p = dev_pool(pool)
     rng, ids, tb = h.bin(p, oH, oW)
     _, tb_ref, _ = O.boxes(opar(pool), H, W, oH, oW)
@@ -229,9 +242,15 @@ def test_render_parity(H, W, C, K, order, scale):
     y_ref, D_ref = O.render(opar(pool), H, W, oH, oW)
     assert (D_ref > 0).mean() > 0.5
     assert_pixels(y, y_ref)
-    # deterministic: the forward has no atomics
+    # deterministic: the forward has no atomics; the float4 store epilogue
+    # writes the same pixels (ragged widths fall back to scalar stores)
     y2 = h.render(dev_pool(pool), oH, oW).cpu().numpy()
     np.testing.assert_array_equal(y, y2)
+    y4 = h.render(dev_pool(pool), oH, oW, vector_stores=True).cpu().numpy()
+    np.testing.assert_array_equal(y, y4)
+    acc = torch.full((C, oH, oW), 0.25, device="cuda")
+    h.render(dev_pool(pool), oH, oW, out=acc, accumulate=0.5, vector_stores=True)
+    np.testing.assert_allclose(acc.cpu().numpy(), 0.25 + 0.5 * y, rtol=1e-6, atol=1e-7)
 
 
 def test_render_host_output_buffer():
@@ -756,7 +775,7 @@ def test_large_grid_unbalanced_buckets_fall_back_to_csr():
     pool = synth.aniso_pool(H, W, 1, K, 63, l_range=(0.3, 0.6), shear=0.1)
     pool.mu[:] = g.uniform(1000.2, 1007.8, (K, 2)).astype(np.float32)
     pool = conditioned(pool, H, W)
-    h = smoe.SMoE(K, H, W, 1, 0)
+    h = smoe.SMoE(K, H, W, 1, 0, box_mode="square")
     p = dev_pool(pool)
     rng, ids, tb = h.bin(p, H, W)
     _, tb_ref, _ = O.boxes(opar(pool), H, W)
@@ -765,3 +784,53 @@ def test_large_grid_unbalanced_buckets_fall_back_to_csr():
     np.testing.assert_array_equal(ids.numpy(), ids_ref)
     st = h.step(p, torch.zeros(1, H, W, device="cuda"), smoe.LR())
     assert np.isfinite(st.loss) and st.pairs == len(ids_ref)
+
+
+# ------------------------------------------------- box modes (reading Q4) --
+
+MODE_CASES = [
+    # H, W, C, K, order, out scale, seed
+    (61, 83, 3, 200, 1, 1.0, 201),
+    (40, 52, 1, 120, 0, 2.0, 202),
+    (70, 45, 3, 300, 0, 0.5, 203),
+]
+
+
+@pytest.mark.parametrize("mode", ["aabb", "exact"])
+@pytest.mark.parametrize("binner", ["direct", "csr_scan_lpt", "csr_coop", "two_stage"])
+@pytest.mark.parametrize("H,W,C,K,order,scale,seed", MODE_CASES)
+def test_box_mode_lists_bit_exact(H, W, C, K, order, scale, seed, mode, binner, monkeypatch):
+    """Box modes aabb / exact through every
+    binner: tile boxes and the canonical lists equal the oracle's
+    (O.block_lists) bit for bit on mode-conditioned anisotropic pools."""
+    for k, v in BINNERS[binner][0].items():
+        monkeypatch.setenv(k, v)
+    oH, oW = int(round(H * scale)), int(round(W * scale))
+    pool = synth.aniso_pool(H, W, C, K, seed, order=order, margin_px=6, l_range=(1.0, 6.0), shear=4.0)
+    pool = conditioned_mode(pool, H, W, oH, oW, mode=mode)
+    h = smoe.SMoE(K, H, W, C, order, box_mode=mode)
+    rng, ids, tb = h.bin(dev_pool(pool), oH, oW)
+    rng_ref, ids_ref, tb_ref = O.block_lists(opar(pool), H, W, oH, oW, mode=mode)
+    np.testing.assert_array_equal(tb.numpy(), tb_ref)
+    np.testing.assert_array_equal(rng.numpy(), rng_ref)
+    np.testing.assert_array_equal(ids.numpy(), ids_ref)
+    sq, _, _ = O.block_lists(opar(pool), H, W, oH, oW, mode="square")
+    assert rng_ref[-1] < sq[-1]                   # fewer pairs than the square box
+
+
+@pytest.mark.parametrize("mode", ["aabb", "exact"])
+def test_box_mode_pixels_and_gradients(mode):
+    """Pixels, loss and gradients do not depend on the box mode: each mode's
+    render and gradients match the oracle (which has no binning at all)."""
+    H, W, C, K = 64, 72, 3, 150
+    pool = synth.aniso_pool(H, W, C, K, 210, order=1, margin_px=5, l_range=(1.0, 6.0), shear=4.0, log_pi_sd=0.3)
+    pool = conditioned_mode(pool, H, W, mode=mode)
+    target = synth.image(H, W, C, 211)
+    h = smoe.SMoE(K, H, W, C, 1, box_mode=mode)
+    y = h.render(dev_pool(pool)).cpu().numpy()
+    y_ref, _ = O.render(opar(pool), H, W)
+    assert_pixels(y, y_ref)
+    g, sums = h.grad(dev_pool(pool), torch.as_tensor(target).cuda())
+    lg = O.loss_grad(opar(pool), target.astype(np.float64))
+    assert abs(float(sums[0]) - lg.sse) <= 1e-5 * lg.sse
+    assert_grads(g.cpu().numpy(), lg.grad, lg.grad_abs, b_ref=lg.grad_opnd)

@@ -637,3 +637,64 @@ def test_operand_scale_bounds_term_scale():
     lz = O.loss_grad(q, np.zeros((3, H, W)))
     m = slice(6, None, 3)                         # m_c components: g eD_c, no inner difference
     np.testing.assert_allclose(lz.grad_opnd[:, m], lz.grad_abs[:, m], rtol=1e-12, atol=0)
+
+
+def test_box_modes_closed_forms_nesting_and_coverage():
+    """Box modes (reading Q4): the aabb half sides are the
+    ellipse's extents R l11 and R sqrt(l21^2 + l22^2) (checked by sampling
+    the ellipse boundary x = mu + R L (cos t, sin t)); the lists nest
+    exact <= aabb <= square; square mode equals the boxes/tile_list route;
+    and every (pixel, kernel) pair inside the ellipse is listed in every
+    mode (coverage invariant), at 1x and at an SR raster."""
+    H, W = 57, 70
+    pool = synth.aniso_pool(H, W, 1, 60, 21, margin_px=6)
+    p = pool_params(pool)
+    R2 = O.R2_99()
+    t = np.linspace(0, 2 * np.pi, 20001)
+    for k in range(5):
+        l11, l21, l22 = p.chol[k]
+        L = np.array([[l11, 0.0], [l21, l22]])
+        pts = np.sqrt(R2) * (L @ np.stack([np.cos(t), np.sin(t)]))
+        assert abs(np.abs(pts[0]).max() - np.sqrt(R2) * l11) < 1e-6
+        assert abs(np.abs(pts[1]).max() - np.sqrt(R2 * (l21 ** 2 + l22 ** 2))) < 1e-6
+    for (oH, oW) in [(H, W), (2 * H, 2 * W), (40, 50)]:
+        lists = {m: O.block_lists(p, H, W, oH, oW, mode=m) for m in ("square", "aabb", "exact")}
+        pairs = {m: set(zip(np.repeat(np.arange(len(r) - 1), np.diff(r)).tolist(), ids.tolist()))
+                 for m, (r, ids, _) in lists.items()}
+        assert pairs["exact"] <= pairs["aabb"] <= pairs["square"]
+        assert len(pairs["exact"]) < len(pairs["square"])
+        _, tb, _ = O.boxes(p, H, W, oH, oW)
+        r0, i0 = O.tile_list(tb, -(-oW // 16), -(-oH // 16))
+        np.testing.assert_array_equal(lists["square"][0], r0)
+        np.testing.assert_array_equal(lists["square"][1], i0)
+        nx = -(-oW // 16)
+        for i in range(oH):
+            for j in range(oW):
+                xs, ys = (j + 0.5) * W / oW - 0.5, (i + 0.5) * H / oH - 0.5
+                tile = (i // 16) * nx + j // 16
+                for k in range(p.K):
+                    if O.d2(p.mu[k], p.chol[k], xs, ys) <= R2:
+                        for m in pairs:
+                            assert (tile, k) in pairs[m], (m, i, j, k)
+
+
+def test_rect_min_d2_against_dense_sampling():
+    """oracle_rect_min_d2 (exact box mode) equals the minimum of d^2 over a
+    fine grid of the rectangle up to the grid's resolution, never exceeds
+    it, and is 0 with the centre inside."""
+    g = np.random.default_rng(4)
+    for _ in range(40):
+        mu = g.uniform(-5, 25, 2)
+        ch = np.array([g.uniform(0.5, 4), g.uniform(-2, 2), g.uniform(0.5, 4)])
+        x0, y0 = g.uniform(0, 10, 2)
+        x1, y1 = x0 + g.uniform(0.5, 15), y0 + g.uniform(0.5, 15)
+        v = O.rect_min_d2(mu, ch, x0, x1, y0, y1)
+        xs, ys = np.meshgrid(np.linspace(x0, x1, 401), np.linspace(y0, y1, 401))
+        L = np.array([[ch[0], 0], [ch[1], ch[2]]])
+        Si = np.linalg.inv(L @ L.T)
+        d = np.stack([xs - mu[0], ys - mu[1]], -1)
+        dense = np.einsum("...i,ij,...j->...", d, Si, d).min()
+        assert v <= dense + 1e-9
+        assert dense - v <= 0.05 * max(1.0, dense)
+        if x0 <= mu[0] <= x1 and y0 <= mu[1] <= y1:
+            assert v == 0.0
