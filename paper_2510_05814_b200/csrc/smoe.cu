@@ -334,6 +334,10 @@ void grow(smoe_ctx *h, Grid &g, long long need)
     dfree(g.ids); dfree(g.tmp);
     CK(cudaMalloc(&g.ids, sizeof(int) * cap));
     CK(cudaMalloc(&g.tmp, sizeof(int) * cap));
+    // defined contents for the slots past a bucket's length (read only by the
+    // smoe_bin diagnostic copy; keeps compute-sanitizer initcheck clean)
+    CK(cudaMemsetAsync(g.ids, 0, sizeof(int) * cap, h->stream));
+    CK(cudaMemsetAsync(g.tmp, 0, sizeof(int) * cap, h->stream));
     g.cap = cap;
     g.calibrated = true;
     CK(cudaMemsetAsync(&g.gc->need, 0, 2 * sizeof(long long), h->stream));  // need, skipped

@@ -1118,6 +1118,9 @@ __device__ __forceinline__ void sort_bucket(int *seg, int n, int *tmp, int *s, i
 {
     if (n <= 1) return;
     if (n <= 256) {
+        // one warp in registers while the other three wait at the next
+        // barrier (a four-warp version -- quarter runs + rank merge by binary
+        // search -- measured 3% slower at configs 2-4: DESIGN.md §10)
         if (threadIdx.x < 32) {
             int lane = threadIdx.x;
             if (n <= 32) warp_sort_seg<1>(seg, n, lane);
