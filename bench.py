@@ -358,7 +358,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="div2k", choices=["tiny", "kodak", "div2k", "denoise", "8k"])
-    ap.add_argument("--cpu-rows", type=int, default=64, help="image rows of the cpu_baseline sample")
+    ap.add_argument("--cpu-rows", type=int, default=0,
+                    help="image rows of the cpu_baseline sample (0: about 15 s of oracle work, from the measured "
+                         "~12 ns per (pixel, kernel) of the dense fp64 loss + gradient)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
@@ -647,7 +649,8 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        rows = min(args.cpu_rows, H)
+        rows = args.cpu_rows or int(round(15.0 / (W * K * 1.2e-8)))
+        rows = max(1, min(rows, H))
         r0 = (H - rows) // 2
         tg, ta, core = cpu_oracle_sample(target, pool, (r0, r0 + rows))
         cpu = dict({"value": 1.0 / (tg * H / rows + ta), "unit": "it/s", "cores": 1, "kind": "oracle",

@@ -260,8 +260,11 @@ preprocess_one(int k, ParamsDev p, float R2, float sx, float sy, int oW, int oH,
                int nx, int ty_lo, int ty_hi, float *__restrict__ rec,
                int4 *__restrict__ tbox, int *__restrict__ cnt, HandleCtr *hc, float lscale, int mode,
                bool direct = false, int *__restrict__ dids = nullptr, int bcap = 0,
-               int *n_emit = nullptr, int *max_len = nullptr)
+               int *n_emit = nullptr, int *max_len = nullptr, int sub = 0, int tpk = 1)
 {
+    // tpk threads per kernel (direct buckets, small pools): thread `sub`
+    // emits the kernel's blocks sub, sub + tpk, ...; thread 0 alone writes
+    // the record, the tile box and the non-finite flag
     using R = Rec<C, E>;
     float2 mu = reinterpret_cast<const float2 *>(p.mu)[k];
     // lscale = sqrt(s) applies the sharpening edit Sigma -> s Sigma (render only)
@@ -279,7 +282,7 @@ preprocess_one(int k, ParamsDev p, float R2, float sx, float sy, int oW, int oH,
     }
 #pragma unroll
     for (int i = R::P; i < R::RS; i++) r[i] = 0.0f;
-    if (!ok) atomicExch((unsigned long long *)&hc->nonfinite, 1ull);
+    if (!ok && sub == 0) atomicExch((unsigned long long *)&hc->nonfinite, 1ull);
 
     float s11 = l11 * l11, s12 = l11 * l21, s22 = l21 * l21 + l22 * l22;
     float rx, ry;
@@ -305,7 +308,7 @@ preprocess_one(int k, ParamsDev p, float R2, float sx, float sy, int oW, int oH,
         // the record is read only through the block lists: write it only for
         // a kernel listed in some block of the band (a multi-GPU rank skips
         // the records of kernels outside its band)
-        if (y0 <= y1) {
+        if (y0 <= y1 && sub == 0) {
             float4 *dst = reinterpret_cast<float4 *>(rec) + (size_t)k * (R::RS / 4);
 #pragma unroll
             for (int q = 0; q < R::RS / 4; q++) dst[q] = make_float4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
@@ -315,12 +318,12 @@ preprocess_one(int k, ParamsDev p, float R2, float sx, float sy, int oW, int oH,
             // fixed-capacity bucket (PRE_ATOM atomics in flight per round)
             const int wx = tb.y - tb.x + 1, nbx = max(0, y1 - y0 + 1) * wx;
             int emitted = 0;
-            for (int i0 = 0; i0 < nbx; i0 += PRE_ATOM) {
+            for (int i0 = sub; i0 < nbx; i0 += PRE_ATOM * tpk) {
                 int t[PRE_ATOM], sl[PRE_ATOM];
                 bool on[PRE_ATOM];
 #pragma unroll
                 for (int q = 0; q < PRE_ATOM; q++) {
-                    const int i = i0 + q, yy = y0 + i / wx, xx = tb.x + i % wx;
+                    const int i = i0 + q * tpk, yy = y0 + i / wx, xx = tb.x + i % wx;
                     t[q] = yy * nx + xx;
                     on[q] = i < nbx && (mode != 2 || block_meets(mu.x, mu.y, a, b, c, xx, yy, G, R2));
                     sl[q] = on[q] ? atomicAdd(&cnt[t[q]], 1) : bcap;
@@ -338,7 +341,7 @@ preprocess_one(int k, ParamsDev p, float R2, float sx, float sy, int oW, int oH,
                     if (mode != 2 || block_meets(mu.x, mu.y, a, b, c, tx, ty, G, R2)) atomicAdd(&cnt[ty * nx + tx], 1);
         }
     }
-    tbox[k] = tb;
+    if (sub == 0) tbox[k] = tb;
 }
 
 constexpr int PRE_NT = 256;
@@ -376,13 +379,17 @@ k_preprocess(int K, ParamsDev p, float R2, float sx /* oW/W */, float sy /* oH/H
              int4 *__restrict__ tbox, int *__restrict__ cnt, HandleCtr *hc,
              int n_tiles, int *__restrict__ start, int *__restrict__ cursor, long long cap,
              GridCtr *gc, double *dstats, int *__restrict__ order, float lscale, int build_order,
-             int *__restrict__ dids, int bcap, int *__restrict__ len, int mode)
+             int *__restrict__ dids, int bcap, int *__restrict__ len, int mode, int tpk)
 {
-    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    // tpk > 1 (direct buckets, small pools): tpk consecutive threads share a
+    // kernel and split its block atomics -- more CTAs in flight and fewer
+    // dependent atomic rounds per thread (the small-pool latency floor)
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+    const int k = gt / tpk, sub = gt - k * tpk;
     int n_emit = 0, max_len = 0;
     if (k < K)
         preprocess_one<C, E>(k, p, R2, sx, sy, oW, oH, nx, ty_lo, ty_hi, rec, tbox, cnt, hc, lscale, mode,
-                             len != nullptr, dids, bcap, &n_emit, &max_len);
+                             len != nullptr, dids, bcap, &n_emit, &max_len, sub, tpk);
     if (len) {
         // direct buckets: this CTA's pairs and longest slot to the grid counters
         __shared__ unsigned long long s_pairs;
