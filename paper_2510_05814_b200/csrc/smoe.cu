@@ -399,9 +399,7 @@ void check_params(const smoe_params *p)
 // Two-stage binning (k_records + k_emit over a spatial kernel order) for
 // large pools on direct-bucket grids: one returning global atomic per
 // (CTA, block) instead of per (kernel, block).  SMOE_PERM=0/1 forces it off/on.
-#ifndef SMOE_RASTER4_DEFAULT
-#define SMOE_RASTER4_DEFAULT 0   // four pixels per lane train raster (k_raster4)
-#endif
+constexpr int RENDER4_MAX_BCAP = 256;   // render form switch (bucket capacity = 1.25 x longest + 32)
 constexpr int PRE_TPK = 8;   // one-pass direct binning: threads per kernel (measured: config 2 +4%, config 1 +3% over 1)
 constexpr int PERM_MIN_K = 16384;   // measured: config 4 (20k) +6%, config 2 (10k) -2%
 constexpr long long PERM_REFRESH = 256;
@@ -684,19 +682,10 @@ void forward_backward(smoe_ctx *h, const smoe_params *p, const float *target)
     A.e_scale = (float)(2.0 / ((double)h->H * h->W * h->C));
     A.acc = h->acc; A.dstats = h->ctl->dstats; A.out = nullptr;
     A.work = h->prof.d_work;
-    const char *r4e = getenv("SMOE_RASTER4");
-    const bool r4 = effective_bwd(h) == 1 && !A.order && (r4e ? atoi(r4e) != 0 : SMOE_RASTER4_DEFAULT);
     launch(h, SMOE_KERNEL_RASTER_TRAIN, "k_raster<train>", [&] {
         bool kp = effective_bwd(h) == 1;
         bool cw = h->prof.on && (h->prof.mask & 0x80000000u);
         const void *f = nullptr;
-        if (r4) {
-            if (cw) DISPATCH_CE(h, (f = (const void *)k_raster4<C_, E_, true>));
-            else DISPATCH_CE(h, (f = (const void *)k_raster4<C_, E_, false>));
-            void *args[1] = {&A};
-            (void)cudaLaunchKernel(f, dim3(nt), dim3(R4_NT), args, 0, h->stream);
-            return;
-        }
         if (cw && kp) DISPATCH_CE(h, (f = (const void *)k_raster<C_, E_, true, true, true>));
         else if (kp) DISPATCH_CE(h, (f = (const void *)k_raster<C_, E_, true, false, true>));
         else if (cw) DISPATCH_CE(h, (f = (const void *)k_raster<C_, E_, true, true, false>));
@@ -1272,8 +1261,21 @@ smoe_status smoe_render_ex(smoe_handle h, const smoe_params *p, int out_H, int o
             A.accum = opt ? opt->accumulate : 0.0f;
             A.vec_out = opt && opt->vector_stores ? 1 : 0;
             A.work = h->prof.d_work;
+            // four pixels per lane for grids whose longest bucket is short
+            // (measured: +6 to +11% at <= ~110 kernels per block, -7% at config
+            // 4's 151); SMOE_RENDER4=0/1 forces either form
+            const char *r4e = getenv("SMOE_RENDER4");
+            const bool r4 = !A.order && !A.vec_out && (r4e ? atoi(r4e) != 0 : (g.direct && g.bcap <= RENDER4_MAX_BCAP));
             launch(h, SMOE_KERNEL_RASTER_RENDER, "k_raster<render>", [&] {
                 const void *f = nullptr;
+                if (r4) {
+                    if (h->prof.on && (h->prof.mask & 0x80000000u))
+                        DISPATCH_CE(h, (f = (const void *)k_render4<C_, E_, true>));
+                    else DISPATCH_CE(h, (f = (const void *)k_render4<C_, E_, false>));
+                    void *args[1] = {&A};
+                    (void)cudaLaunchKernel(f, dim3(g.n_tiles), dim3(R4_NT), args, 0, h->stream);
+                    return;
+                }
                 if (h->prof.on && (h->prof.mask & 0x80000000u))
                     DISPATCH_CE(h, (f = (const void *)k_raster<C_, E_, false, true, false>));
                 else DISPATCH_CE(h, (f = (const void *)k_raster<C_, E_, false, false, false>));

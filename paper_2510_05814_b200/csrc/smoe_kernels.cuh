@@ -1756,35 +1756,27 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
     release();
 }
 
-// ------------------------------------------- a4-a7, four pixels per lane --
-// Training raster with two warps per 16x16 block: warp w covers columns
+// ------------------------------------------- a4, a5, a9: four pixels per lane --
+// Render raster with two warps per 16x16 block: warp w covers columns
 // [8w, 8w+8), lane l the vertical strip of four pixels (8w + (l & 7),
 // 4 (l >> 3) + {0..3}).  The four pixels share dx, so per (warp, kernel) the
 // test costs ~23 instructions for 128 pixels (two packed f32x2 pairs in dy)
-// instead of ~34 for two 64-pixel warps, and the backward's per-entry decode,
-// record and kernel-switch costs are shared by up to four pixels.  Same
-// arithmetic per pixel as raster_tile (forward sums, seeds, raw sums of gG),
-// same lists, same kernel-parallel backward over per-(warp, kernel) ballot
-// records (four ballots per record).
+// instead of ~34 for two 64-pixel warps of raster_tile.  Same per-pixel
+// arithmetic and list order as raster_tile's render (identical pixels).
+// Measured: config 3 4x SR +11%, configs 2/5 1x +6%, but config 4 1x (151
+// kernels per block) -7% -- the host picks this form for grids whose
+// longest bucket is short.  The same layout for the TRAIN
+// raster (seeds and kernel-parallel backward over four-ballot records) was
+// built, passed the parity suite and measured 8-26% slower (§10).
 constexpr int R4_NT = 64;
-#ifndef SMOE_R4_MINB
-#define SMOE_R4_MINB 12
-#endif
 
 template <int C, int E, bool PROF>
-__device__ __forceinline__ void raster_tile4(const RasterArgs &A, const int tile)
+__device__ __forceinline__ void render_tile4(const RasterArgs &A, const int tile)
 {
     using R = Rec<C, E>;
     constexpr int RS4 = R::RS / 4;
     constexpr int BATCH = SMOE_RASTER_BATCH;
-    constexpr int NS = C + 1;                       // seed float4s per lane: eD_c (4 px) ..., K (4 px)
     __shared__ float4 srec[BATCH * RS4];
-    __shared__ int sid[BATCH];
-    __shared__ float4 spix[R4_NT * NS];
-    __shared__ float2 sxy[R4_NT];
-    __shared__ uint4 skb[2][BATCH];                 // per (warp, kernel): the four row ballots
-    __shared__ uint2 skm[2][BATCH];                 // kernel slot in the batch, entries before it
-    __shared__ double red[3][2];
 
     const int tx = tile % A.nx, ty = tile / A.nx;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1793,19 +1785,14 @@ __device__ __forceinline__ void raster_tile4(const RasterArgs &A, const int tile
     bool vv[4];
 #pragma unroll
     for (int i = 0; i < 4; i++) vv[i] = px < A.oW && py + i < A.oH;
-    const float xs = (float)px;
-    const float2 ys01 = make_float2((float)py, (float)(py + 1)), ys23 = make_float2((float)(py + 2), (float)(py + 3));
+    // source coordinates of the output samples (Q16)
+    const float xs = (px + 0.5f) * A.sx - 0.5f;
+    const float2 ys01 = make_float2((py + 0.5f) * A.sy - 0.5f, (py + 1.5f) * A.sy - 0.5f);
+    const float2 ys23 = make_float2((py + 2.5f) * A.sy - 0.5f, (py + 3.5f) * A.sy - 0.5f);
     const float R2 = A.R2;
     const int s0 = A.len ? tile * A.bcap : A.start[tile];
     const int n = A.len ? A.len[tile] : A.start[tile + 1] - s0;
     const long long c_start = PROF ? clock64() : 0;
-    auto release = [&] {
-        if (A.len && threadIdx.x == 0) {
-            A.lenout[tile] = n;
-            if (n) A.len[tile] = 0;
-        }
-        if (PROF && threadIdx.x == 0) atomicAdd(&A.work[3], (unsigned long long)(clock64() - c_start));
-    };
     constexpr int SCHUNK = (BATCH * RS4 * 4 >= 2048) ? 2048 : 1024;
     sort_bucket(A.ids + s0, n, A.tmp + s0, reinterpret_cast<int *>(srec), SCHUNK);
     if (PROF) {
@@ -1816,313 +1803,109 @@ __device__ __forceinline__ void raster_tile4(const RasterArgs &A, const int tile
 #pragma unroll
     for (int c = 0; c < C; c++) { N01[c] = D01; N23[c] = D01; }
     unsigned long long w_tested = 0, w_hit = 0;
-    int wrun = 0, nrec = 0;
     int w_valid = 0;
     if (PROF) {
 #pragma unroll
         for (int i = 0; i < 4; i++) w_valid += __popc(__ballot_sync(FULL, vv[i]));
     }
-    auto load_batch = [&](int b0, int nb) {
+    for (int b0 = 0; b0 < n; b0 += BATCH) {
+        const int nb = min(BATCH, n - b0);
         __syncthreads();
         for (int i = threadIdx.x; i < nb * RS4; i += blockDim.x) {
-            int j = i / RS4, q = i - j * RS4;
-            int id = A.ids[s0 + b0 + j];
-            srec[i] = reinterpret_cast<const float4 *>(A.rec)[(size_t)id * RS4 + q];
-            if (q == 0) sid[j] = id;
+            const int j = i / RS4, q = i - j * RS4;
+            srec[i] = reinterpret_cast<const float4 *>(A.rec)[(size_t)A.ids[s0 + b0 + j] * RS4 + q];
         }
         __syncthreads();
-    };
-    auto load_rec = [&](int j, float (&r)[R::RS]) {
-#pragma unroll
-        for (int q = 0; q < RS4; q++) {
-            float4 f = srec[j * RS4 + q];
-            r[4 * q] = f.x; r[4 * q + 1] = f.y; r[4 * q + 2] = f.z; r[4 * q + 3] = f.w;
-        }
-    };
-    // d^2 of the lane's four pixels for record r (dx shared, dy as two pairs)
-    auto dist4 = [&](const float (&r)[R::RS], float &dx, float2 &dy01, float2 &dy23, float &u, float2 &w01,
-                     float2 &w23, float2 &q01, float2 &q23) {
-        dx = xs - r[0];
-        dy01 = __fadd2_rn(ys01, make_float2(-r[1], -r[1]));
-        dy23 = __fadd2_rn(ys23, make_float2(-r[1], -r[1]));
-        u = r[2] * dx;
-        const float bdx = r[3] * dx, uu = u * u;
-        w01 = __ffma2_rn(make_float2(r[4], r[4]), dy01, make_float2(bdx, bdx));
-        w23 = __ffma2_rn(make_float2(r[4], r[4]), dy23, make_float2(bdx, bdx));
-        q01 = __ffma2_rn(w01, w01, make_float2(uu, uu));
-        q23 = __ffma2_rn(w23, w23, make_float2(uu, uu));
-    };
-    auto ballots = [&](const float2 &q01, const float2 &q23, unsigned (&bm)[4], bool (&h)[4]) {
-        h[0] = vv[0] && q01.x <= R2; h[1] = vv[1] && q01.y <= R2;
-        h[2] = vv[2] && q23.x <= R2; h[3] = vv[3] && q23.y <= R2;
-#pragma unroll
-        for (int i = 0; i < 4; i++) bm[i] = __ballot_sync(FULL, h[i]);
-    };
-
-    // ---- forward (Eq. 5 with the per-pixel cull of P:221) ----
-    auto forward = [&](auto list_tag) {
-        constexpr bool LIST = decltype(list_tag)::value;
-        for (int b0 = 0; b0 < n; b0 += BATCH) {
-            int nb = min(BATCH, n - b0);
-            load_batch(b0, nb);
 #pragma unroll 1
-            for (int j = 0; j < nb; j++) {
-                float r[R::RS];
-                load_rec(j, r);
-                float dx, u;
-                float2 dy01, dy23, w01, w23, q01, q23;
-                dist4(r, dx, dy01, dy23, u, w01, w23, q01, q23);
-                unsigned bm[4];
-                bool h[4];
-                ballots(q01, q23, bm, h);
-                const unsigned any = bm[0] | bm[1] | bm[2] | bm[3];
-                if (PROF) {
-                    w_tested += w_valid;
-                    w_hit += __popc(bm[0]) + __popc(bm[1]) + __popc(bm[2]) + __popc(bm[3]);
-                }
-                if (any == 0u) continue;
-                if (LIST) {
-                    if (lane == 0) {
-                        skb[warp][nrec] = make_uint4(bm[0], bm[1], bm[2], bm[3]);
-                        skm[warp][nrec] = make_uint2((unsigned)j, (unsigned)wrun);
-                    }
-                    nrec++;
-                    wrun += __popc(any);
-                }
-                const float2 L = make_float2(-0.5f * LOG2E, -0.5f * LOG2E), lp = make_float2(r[5], r[5]);
-                const float2 e01 = __ffma2_rn(q01, L, lp), e23 = __ffma2_rn(q23, L, lp);
-                const float2 g01 = make_float2(h[0] ? ex2_approx(e01.x) : 0.f, h[1] ? ex2_approx(e01.y) : 0.f);
-                const float2 g23 = make_float2(h[2] ? ex2_approx(e23.x) : 0.f, h[3] ? ex2_approx(e23.y) : 0.f);
-                D01 = __fadd2_rn(D01, g01);
-                D23 = __fadd2_rn(D23, g23);
+        for (int j = 0; j < nb; j++) {
+            float r[R::RS];
 #pragma unroll
-                for (int c = 0; c < C; c++) {
-                    float2 m01 = make_float2(r[6 + c * E], r[6 + c * E]), m23 = m01;
-                    if (E == 3) {
-                        const float mb = fmaf(r[6 + c * E + 1], dx, r[6 + c * E]);
-                        const float2 wy = make_float2(r[6 + c * E + 2], r[6 + c * E + 2]);
-                        m01 = __ffma2_rn(wy, dy01, make_float2(mb, mb));
-                        m23 = __ffma2_rn(wy, dy23, make_float2(mb, mb));
-                    }
-                    N01[c] = __ffma2_rn(g01, m01, N01[c]);
-                    N23[c] = __ffma2_rn(g23, m23, N23[c]);
+            for (int q = 0; q < RS4; q++) {
+                const float4 f = srec[j * RS4 + q];
+                r[4 * q] = f.x; r[4 * q + 1] = f.y; r[4 * q + 2] = f.z; r[4 * q + 3] = f.w;
+            }
+            const float dx = xs - r[0];
+            const float2 dy01 = __fadd2_rn(ys01, make_float2(-r[1], -r[1]));
+            const float2 dy23 = __fadd2_rn(ys23, make_float2(-r[1], -r[1]));
+            const float u = r[2] * dx, bdx = r[3] * dx, uu = u * u;
+            const float2 w01 = __ffma2_rn(make_float2(r[4], r[4]), dy01, make_float2(bdx, bdx));
+            const float2 w23 = __ffma2_rn(make_float2(r[4], r[4]), dy23, make_float2(bdx, bdx));
+            const float2 q01 = __ffma2_rn(w01, w01, make_float2(uu, uu));
+            const float2 q23 = __ffma2_rn(w23, w23, make_float2(uu, uu));
+            const bool h0 = vv[0] && q01.x <= R2, h1 = vv[1] && q01.y <= R2;
+            const bool h2 = vv[2] && q23.x <= R2, h3 = vv[3] && q23.y <= R2;
+            if (PROF) {
+                w_tested += w_valid;
+                w_hit += __popc(__ballot_sync(FULL, h0)) + __popc(__ballot_sync(FULL, h1)) +
+                         __popc(__ballot_sync(FULL, h2)) + __popc(__ballot_sync(FULL, h3));
+            }
+            if (!__any_sync(FULL, h0 || h1 || h2 || h3)) continue;
+            const float2 L = make_float2(-0.5f * LOG2E, -0.5f * LOG2E), lp = make_float2(r[5], r[5]);
+            const float2 e01 = __ffma2_rn(q01, L, lp), e23 = __ffma2_rn(q23, L, lp);
+            const float2 g01 = make_float2(h0 ? ex2_approx(e01.x) : 0.f, h1 ? ex2_approx(e01.y) : 0.f);
+            const float2 g23 = make_float2(h2 ? ex2_approx(e23.x) : 0.f, h3 ? ex2_approx(e23.y) : 0.f);
+            D01 = __fadd2_rn(D01, g01);
+            D23 = __fadd2_rn(D23, g23);
+#pragma unroll
+            for (int c = 0; c < C; c++) {
+                float2 m01 = make_float2(r[6 + c * E], r[6 + c * E]), m23 = m01;
+                if (E == 3) {
+                    const float mb = fmaf(r[6 + c * E + 1], dx, r[6 + c * E]);
+                    const float2 wy = make_float2(r[6 + c * E + 2], r[6 + c * E + 2]);
+                    m01 = __ffma2_rn(wy, dy01, make_float2(mb, mb));
+                    m23 = __ffma2_rn(wy, dy23, make_float2(mb, mb));
                 }
+                N01[c] = __ffma2_rn(g01, m01, N01[c]);
+                N23[c] = __ffma2_rn(g23, m23, N23[c]);
             }
         }
-    };
-    if (n <= BATCH) forward(std::true_type{});
-    else forward(std::false_type{});
+    }
     if (PROF && lane == 0) {
         atomicAdd(&A.work[0], w_tested);
         atomicAdd(&A.work[1], w_hit);
     }
-    // y = N/D (SMoE) or N (RBF head); loss partials; seeds eD_c, K per pixel
+    // y = N/D (SMoE) or N (RBF head); each lane stores its strip (a warp
+    // store covers 8 rows x 32 contiguous bytes)
     const float Dv[4] = {D01.x, D01.y, D23.x, D23.y};
-    float iD[4], y[4][C];
+    const size_t plane = (size_t)A.oH * A.oW;
 #pragma unroll
-    for (int i = 0; i < 4; i++) iD[i] = A.rbf ? 1.f : (Dv[i] > 0.f ? 1.0f / Dv[i] : 0.f);
+    for (int i = 0; i < 4; i++) {
+        if (!vv[i]) continue;
+        const float iD = A.rbf ? 1.f : (Dv[i] > 0.f ? 1.0f / Dv[i] : 0.f);
+        float *o = A.out + (size_t)(py + i) * A.oW + px;
 #pragma unroll
-    for (int c = 0; c < C; c++) {
-        y[0][c] = N01[c].x * iD[0]; y[1][c] = N01[c].y * iD[1];
-        y[2][c] = N23[c].x * iD[2]; y[3][c] = N23[c].y * iD[3];
-    }
-    {
-        float sse = 0.f, ssec = 0.f, unc = 0.f;
-        const size_t plane = (size_t)A.oH * A.oW;
-        float ed[C][4], Kk[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int i = 0; i < 4; i++) {
-#pragma unroll
-            for (int c = 0; c < C; c++) {
-                const float t = vv[i] ? A.target[c * plane + (size_t)(py + i) * A.oW + px] : 0.f;
-                const float rr = vv[i] ? y[i][c] - t : 0.f;
-                const float rc = vv[i] ? __saturatef(y[i][c]) - __saturatef(t) : 0.f;
-                sse = fmaf(rr, rr, sse);
-                ssec = fmaf(rc, rc, ssec);
-                ed[c][i] = A.e_scale * rr * iD[i];
-                if (!A.rbf) Kk[i] = fmaf(ed[c][i], y[i][c], Kk[i]);
-            }
-            unc += (vv[i] && Dv[i] <= 0.f) ? 1.f : 0.f;
-        }
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) {
-            sse += __shfl_xor_sync(FULL, sse, o);
-            ssec += __shfl_xor_sync(FULL, ssec, o);
-            unc += __shfl_xor_sync(FULL, unc, o);
-        }
-        if (lane == 0) { red[0][warp] = (double)sse; red[1][warp] = (double)ssec; red[2][warp] = (double)unc; }
-        float4 *sp = spix + NS * threadIdx.x;
-#pragma unroll
-        for (int c = 0; c < C; c++) sp[c] = make_float4(ed[c][0], ed[c][1], ed[c][2], ed[c][3]);
-        sp[C] = make_float4(Kk[0], Kk[1], Kk[2], Kk[3]);
-        sxy[threadIdx.x] = make_float2(xs, (float)py);
-        __syncthreads();
-        if (threadIdx.x < 3) {
-            const double sm = red[threadIdx.x][0] + red[threadIdx.x][1];
-            if (sm != 0.0) atomicAdd(&A.dstats[threadIdx.x], sm);
+        for (int c = 0; c < C; c++) {
+            const float2 Nc = (i < 2) ? N01[c] : N23[c];
+            const float y = ((i & 1) ? Nc.y : Nc.x) * iD;
+            o[c * plane] = A.accum != 0.f ? fmaf(A.accum, y, o[c * plane]) : y;
         }
     }
-
-    // ---- kernel-parallel backward over the per-warp ballot records ----
-    const unsigned spw = (unsigned)__cvta_generic_to_shared(spix + warp * 32 * NS);
-    const unsigned sxyw = (unsigned)__cvta_generic_to_shared(sxy + warp * 32);
-    const unsigned srec_s = (unsigned)__cvta_generic_to_shared(srec), sid_s = (unsigned)__cvta_generic_to_shared(sid);
-    for (int b0 = 0; b0 < n; b0 += BATCH) {
-        int nb = min(BATCH, n - b0);
-        int total = wrun, nr = nrec;
-        if (n > BATCH) {
-            load_batch(b0, nb);
-            total = 0;
-            nr = 0;
-            for (int j = 0; j < nb; j++) {
-                float rb[R::RS];
-                load_rec(j, rb);
-                float dx, u;
-                float2 dy01, dy23, w01, w23, q01, q23;
-                dist4(rb, dx, dy01, dy23, u, w01, w23, q01, q23);
-                unsigned bm[4];
-                bool h[4];
-                ballots(q01, q23, bm, h);
-                const unsigned any = bm[0] | bm[1] | bm[2] | bm[3];
-                if (any == 0u) continue;
-                if (lane == 0) {
-                    skb[warp][nr] = make_uint4(bm[0], bm[1], bm[2], bm[3]);
-                    skm[warp][nr] = make_uint2((unsigned)j, (unsigned)total);
-                }
-                nr++;
-                total += __popc(any);
-            }
-        }
-        __syncwarp();
-        const int lo = (lane * total) >> 5, hi = ((lane + 1) * total) >> 5;
-        if (lo < hi) {
-            int ra = 0;
-            for (int step = BATCH / 2; step >= 1; step >>= 1)
-                if (ra + step < nr && (int)skm[warp][ra + step].y <= lo) ra += step;
-            uint4 kb = skb[warp][ra];
-            unsigned m = kb.x | kb.y | kb.z | kb.w;
-            {
-                const int k = lo - (int)skm[warp][ra].y;
-                int t = 0;
-#pragma unroll
-                for (int sft = 16; sft >= 1; sft >>= 1)
-                    if (__popc(m & ((1u << (t + sft)) - 1u)) <= k) t += sft;
-                m &= ~((1u << t) - 1u);
-            }
-            float4 *dst;
-            float r[R::RS];
-            float acc[R::P];
-#pragma unroll
-            for (int i = 0; i < R::P; i++) acc[i] = 0.f;
-            auto open_kernel = [&](int j) {
-                dst = reinterpret_cast<float4 *>(A.acc + (size_t)lds32(sid_s + 4u * j) * R::V);
-#pragma unroll
-                for (int q4 = 0; q4 < RS4; q4++) {
-                    const float4 f = lds128(srec_s + 16u * (j * RS4 + q4));
-                    r[4 * q4] = f.x; r[4 * q4 + 1] = f.y; r[4 * q4 + 2] = f.z; r[4 * q4 + 3] = f.w;
-                }
-            };
-            auto flush = [&] {
-#pragma unroll
-                for (int q4 = 0; q4 < (R::P + 3) / 4; q4++) {
-                    float t4[4];
-#pragma unroll
-                    for (int k4 = 0; k4 < 4; k4++) t4[k4] = (4 * q4 + k4 < R::P) ? acc[4 * q4 + k4] : 0.f;
-                    atomicAdd(dst + q4, make_float4(t4[0], t4[1], t4[2], t4[3]));
-                }
-            };
-            open_kernel((int)skm[warp][ra].x);
-            for (int q = lo; q < hi; q++) {
-                if (m == 0u) {
-                    flush();
-#pragma unroll
-                    for (int i = 0; i < R::P; i++) acc[i] = 0.f;
-                    ++ra;
-                    kb = skb[warp][ra];
-                    m = kb.x | kb.y | kb.z | kb.w;
-                    open_kernel((int)skm[warp][ra].x);
-                }
-                const unsigned lb = m & (0u - m);
-                m ^= lb;
-                const int l = 31 - __clz(lb);
-                const bool h0 = (kb.x & lb) != 0u, h1 = (kb.y & lb) != 0u, h2 = (kb.z & lb) != 0u,
-                           h3 = (kb.w & lb) != 0u;
-                const unsigned sa = spw + (unsigned)l * (16u * NS);
-                float2 ed01[C], ed23[C];
-#pragma unroll
-                for (int c = 0; c < C; c++) {
-                    const float4 e = lds128(sa + 16u * c);
-                    ed01[c] = make_float2(e.x, e.y);
-                    ed23[c] = make_float2(e.z, e.w);
-                }
-                const float4 kk = lds128(sa + 16u * C);
-                const float2 xy = lds64(sxyw + 8u * l);
-                const float2 dd = __fadd2_rn(xy, make_float2(-r[0], -r[1]));
-                const float dx = dd.x;
-                const float2 dy01 = __fadd2_rn(make_float2(dd.y, dd.y), make_float2(0.f, 1.f));
-                const float2 dy23 = __fadd2_rn(make_float2(dd.y, dd.y), make_float2(2.f, 3.f));
-                const float u = r[2] * dx, bdx = r[3] * dx, uu = u * u;
-                const float2 v01 = __ffma2_rn(make_float2(r[4], r[4]), dy01, make_float2(bdx, bdx));
-                const float2 v23 = __ffma2_rn(make_float2(r[4], r[4]), dy23, make_float2(bdx, bdx));
-                const float2 q01 = __ffma2_rn(v01, v01, make_float2(uu, uu));
-                const float2 q23 = __ffma2_rn(v23, v23, make_float2(uu, uu));
-                const float2 L = make_float2(-0.5f * LOG2E, -0.5f * LOG2E), lpv = make_float2(r[5], r[5]);
-                const float2 e01 = __ffma2_rn(q01, L, lpv), e23 = __ffma2_rn(q23, L, lpv);
-                const float2 g01 = make_float2(h0 ? ex2_approx(e01.x) : 0.f, h1 ? ex2_approx(e01.y) : 0.f);
-                const float2 g23 = make_float2(h2 ? ex2_approx(e23.x) : 0.f, h3 ? ex2_approx(e23.y) : 0.f);
-                float2 G01 = make_float2(-kk.x, -kk.y), G23 = make_float2(-kk.z, -kk.w);
-#pragma unroll
-                for (int c = 0; c < C; c++) {
-                    float2 m01 = make_float2(r[6 + c * E], r[6 + c * E]), m23 = m01;
-                    if (E == 3) {
-                        const float mb = fmaf(r[6 + c * E + 1], dx, r[6 + c * E]);
-                        const float2 wy = make_float2(r[6 + c * E + 2], r[6 + c * E + 2]);
-                        m01 = __ffma2_rn(wy, dy01, make_float2(mb, mb));
-                        m23 = __ffma2_rn(wy, dy23, make_float2(mb, mb));
-                    }
-                    G01 = __ffma2_rn(ed01[c], m01, G01);
-                    G23 = __ffma2_rn(ed23[c], m23, G23);
-                    const float2 ge01 = __fmul2_rn(g01, ed01[c]), ge23 = __fmul2_rn(g23, ed23[c]);
-                    const float2 gp = __fadd2_rn(ge01, ge23);
-                    const float gs = gp.x + gp.y;
-                    acc[6 + c * E] += gs;
-                    if (E == 3) {
-                        acc[6 + c * E + 1] = fmaf(gs, dx, acc[6 + c * E + 1]);
-                        const float2 gy = __ffma2_rn(ge23, dy23, __fmul2_rn(ge01, dy01));
-                        acc[6 + c * E + 2] += gy.x + gy.y;
-                    }
-                }
-                const float2 gG01 = __fmul2_rn(g01, G01), gG23 = __fmul2_rn(g23, G23);
-                const float2 gp = __fadd2_rn(gG01, gG23);
-                const float gs = gp.x + gp.y;
-                const float2 sv01 = __fmul2_rn(gG01, v01), sv23 = __fmul2_rn(gG23, v23);
-                const float2 vp = __fadd2_rn(sv01, sv23);
-                const float vs = vp.x + vp.y;
-                const float2 yp = __ffma2_rn(sv23, dy23, __fmul2_rn(sv01, dy01));
-                acc[0] = fmaf(gs, u, acc[0]);
-                acc[1] += vs;
-                acc[2] = fmaf(gs, u * dx, acc[2]);
-                acc[3] = fmaf(vs, dx, acc[3]);
-                acc[4] += yp.x + yp.y;
-                acc[5] += gs;
-            }
-            flush();
-        }
-        __syncthreads();
+    if (A.len && threadIdx.x == 0) {
+        A.lenout[tile] = n;
+        if (n) A.len[tile] = 0;
     }
-    release();
+    if (PROF && threadIdx.x == 0) atomicAdd(&A.work[3], (unsigned long long)(clock64() - c_start));
 }
 
 template <int C, int E, bool PROF>
-__global__ void __launch_bounds__(R4_NT, SMOE_R4_MINB)
-k_raster4(RasterArgs A)
+__global__ void __launch_bounds__(R4_NT, 16)
+k_render4(RasterArgs A)
 {
     const int tile = A.tile0 + blockIdx.x;
     if (A.gc->skip) {
         if (A.len && threadIdx.x == 0) A.len[tile] = 0;
+        if (A.out) {
+            const int tx = tile % A.nx, ty = tile / A.nx;
+            const size_t plane = (size_t)A.oH * A.oW;
+            for (int i = threadIdx.x; i < TILE * TILE; i += blockDim.x) {
+                const int x = tx * TILE + (i & (TILE - 1)), y = ty * TILE + i / TILE;
+                if (x < A.oW && y < A.oH)
+                    for (int c = 0; c < C; c++) A.out[c * plane + (size_t)y * A.oW + x] = __int_as_float(0x7fc00000);
+            }
+        }
         return;
     }
-    raster_tile4<C, E, PROF>(A, tile);
+    render_tile4<C, E, PROF>(A, tile);
 }
 
 // Raster grid: one CTA per block.  CTAs take the blocks in the LPT order
