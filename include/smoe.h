@@ -176,6 +176,19 @@ smoe_status smoe_render_ex(smoe_handle h, const smoe_params *p, int out_H, int o
 smoe_status smoe_step(smoe_handle h, smoe_params *p, const float *target,
                       const smoe_lr *lr, smoe_stats *stats);
 
+/* Fused records: when the training grid uses the two-stage
+ * binning, the Adam update of smoe_step also writes the next step's kernel
+ * records and tile boxes (the geometry of P:215-221) for the parameters it
+ * just updated, and the next smoe_step / smoe_grad on the SAME parameter
+ * buffers, band and box mode skips that preprocessing pass.  The library
+ * notices its own calls that change parameters, records or band
+ * (smoe_apply(_ex), smoe_render(_ex), smoe_bin, smoe_set_band, a failed
+ * call); a caller that writes the parameter buffers itself between steps
+ * must call smoe_invalidate first (the Python binding does this from the
+ * tensors' version counters).  No arguments besides the handle; never fails
+ * on a valid handle. */
+smoe_status smoe_invalidate(smoe_handle h);
+
 /* Multi-GPU band split (tile-row bands): restrict
  * smoe_grad to block rows [tile_row0, tile_row1) of the ceil(H/16) rows.
  * The loss normalisation stays 1/(H W C) of the full image, so per-band

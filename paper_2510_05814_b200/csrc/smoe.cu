@@ -69,11 +69,12 @@ struct AdamArgs {
     HandleCtr *hc;
     const GridCtr *gc;
     long long cap;
-    void *ptrs[11];
+    RecOut ro;
+    void *ptrs[12];
     void bind()
     {
-        void *a[11] = {&cm, &pm, &acc, &gin, &gout, &m1, &m2, &lr, &hc, &gc, &cap};
-        for (int i = 0; i < 11; i++) ptrs[i] = a[i];
+        void *a[12] = {&cm, &pm, &acc, &gin, &gout, &m1, &m2, &lr, &hc, &gc, &cap, &ro};
+        for (int i = 0; i < 12; i++) ptrs[i] = a[i];
     }
 };
 
@@ -88,6 +89,8 @@ struct StepGraph {
     int b0 = 0, b1 = 0, bwd = 0;
     bool prof = false;
     unsigned pmask = 0;
+    bool warm = false;    // k_records omitted (records written by the previous Adam)
+    bool fused = false;   // the Adam node writes the next step's records
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     cudaGraphNode_t adam = nullptr;
@@ -147,6 +150,15 @@ struct smoe_ctx {
     bool perm_valid = false;
     long long perm_age = 0;
     const void *perm_mu = nullptr;
+    // fused records: the step's Adam wrote the next step's records and tile
+    // boxes (training grid) for the parameters it updated; the next binning
+    // of the same parameters and band skips k_records.  Any call that writes
+    // the records, the parameters or the band clears it (invalidate_rec).
+    bool rec_fresh = false;
+    bool skip_records = false;
+    bool fuse_now = false;      // the current sequence's Adam writes the records
+    const void *rec_key[4] = {nullptr, nullptr, nullptr, nullptr};
+    int rec_b0 = 0, rec_b1 = 0, rec_mode = 0;
     bool use_graphs = true;
     bool capturing = false;
     cudaStream_t cap_stream = nullptr;
@@ -190,6 +202,7 @@ smoe_status guard(smoe_ctx *h, F &&f)
         if (h) CK(cudaSetDevice(h->device));
         return f();
     } catch (SmoeError &e) {
+        if (h) h->rec_fresh = false;
         set_err(h, e.what());
         return e.st;
     } catch (std::bad_alloc &) {
@@ -323,6 +336,7 @@ void ensure_grid(smoe_ctx *h, Grid &g, GridCtr *gc, int oH, int oW)
 
 void grow(smoe_ctx *h, Grid &g, long long need)
 {
+    h->rec_fresh = false;   // the redo bins from scratch
     long long cap = need + need / 4 + 4096;
     if (g.direct) {
         // need = the longest bucket; every block gets the same capacity
@@ -452,11 +466,12 @@ void bin_unfused(smoe_ctx *h, Grid &g, const smoe_params *p, int ty_lo, int ty_h
     if (two_stage(h, g) && h->perm_valid) {
         float sx = (float)g.oW / (float)h->W, sy = (float)g.oH / (float)h->H;
         const int nb = (K + PRE_NT - 1) / PRE_NT;
-        launch(h, SMOE_KERNEL_PREPROCESS, "k_records", [&] {
-            DISPATCH_CE(h, (k_records<C_, E_><<<nb, PRE_NT, 0, h->stream>>>(
-                               K, pdev(p), h->R2, sx, sy, g.oW, g.oH, g.nx, ty_lo, ty_hi, h->rec, h->tbox,
-                               &h->ctl->hc, lscale, h->box_mode)));
-        });
+        if (!(&g == &h->train && h->skip_records))
+            launch(h, SMOE_KERNEL_PREPROCESS, "k_records", [&] {
+                DISPATCH_CE(h, (k_records<C_, E_><<<nb, PRE_NT, 0, h->stream>>>(
+                                   K, pdev(p), h->R2, sx, sy, g.oW, g.oH, g.nx, ty_lo, ty_hi, h->rec, h->tbox,
+                                   &h->ctl->hc, lscale, h->box_mode)));
+            });
         const int ne = (K + EMIT_NT - 1) / EMIT_NT;
         launch(h, SMOE_KERNEL_EMIT, "k_emit", [&] {
             k_emit<<<ne, EMIT_NT, 0, h->stream>>>(K, h->perm, h->tbox, g.nx, ty_lo, ty_hi, g.cnt, g.ids, g.bcap,
@@ -719,8 +734,41 @@ void *adam_func(smoe_ctx *h, int mode)
     return f;
 }
 
+// Fused records: on when the training grid uses the two-stage
+// binning (SMOE_FUSE_REC=0 turns it off).
+bool fuse_rec(smoe_ctx *h)
+{
+    const char *e = getenv("SMOE_FUSE_REC");
+    const bool on = !e || atoi(e) != 0;
+    return on && h->train.calibrated && h->train.oH == h->H && h->train.oW == h->W && two_stage(h, h->train) &&
+           h->perm_valid;
+}
+
+RecOut rec_out(smoe_ctx *h)
+{
+    int ty_lo, ty_hi;
+    band_rows(h, ty_lo, ty_hi);
+    return RecOut{h->rec, h->tbox, h->R2, h->W, h->H, ty_lo, ty_hi, h->box_mode};
+}
+
+bool rec_is_fresh(const smoe_ctx *h, const smoe_params *p)
+{
+    return h->rec_fresh && h->rec_key[0] == p->mu && h->rec_key[1] == p->chol && h->rec_key[2] == p->log_pi &&
+           h->rec_key[3] == p->expert && h->rec_b0 == h->band0 && h->rec_b1 == h->band1 &&
+           h->rec_mode == h->box_mode;
+}
+
+void mark_rec_fresh(smoe_ctx *h, const smoe_params *p)
+{
+    h->rec_fresh = true;
+    h->rec_key[0] = p->mu; h->rec_key[1] = p->chol; h->rec_key[2] = p->log_pi; h->rec_key[3] = p->expert;
+    h->rec_b0 = h->band0; h->rec_b1 = h->band1; h->rec_mode = h->box_mode;
+}
+
+void invalidate_rec(smoe_ctx *h) { h->rec_fresh = false; }
+
 void adam_args(smoe_ctx *h, const smoe_params *p, const float *grad_in, float *grad_out, const smoe_lr *lr,
-               AdamArgs &a, int k0 = 0, int n = -1, const double *skip_in = nullptr)
+               AdamArgs &a, int k0 = 0, int n = -1, const double *skip_in = nullptr, bool fused = false)
 {
     a.cm.Ktot = h->K;
     a.cm.k0 = k0;
@@ -737,14 +785,15 @@ void adam_args(smoe_ctx *h, const smoe_params *p, const float *grad_in, float *g
     a.hc = &h->ctl->hc;
     a.gc = &h->ctl->train;
     a.cap = h->train.cap;
+    a.ro = fused ? rec_out(h) : RecOut{nullptr, nullptr, 0.f, 0, 0, 0, 0, 0};
     a.bind();
 }
 
 void launch_adam(smoe_ctx *h, int mode, const smoe_params *p, const float *grad_in, float *grad_out,
-                 const smoe_lr *lr, int k0 = 0, int n = -1, const double *skip_in = nullptr)
+                 const smoe_lr *lr, int k0 = 0, int n = -1, const double *skip_in = nullptr, bool fused = false)
 {
     AdamArgs a;
-    adam_args(h, p, grad_in, grad_out, lr, a, k0, n, skip_in);
+    adam_args(h, p, grad_in, grad_out, lr, a, k0, n, skip_in, fused);
     void *f = adam_func(h, mode);
     dim3 grid, block;
     const int cnt = std::max(1, a.cm.n);
@@ -813,7 +862,8 @@ bool graph_matches(smoe_ctx *h, const StepGraph &g, const smoe_params *p, const 
     return g.valid && g.mu == p->mu && g.chol == p->chol && g.lp == p->log_pi && g.ex == p->expert &&
            g.target == t && g.gout == gout && g.ids == h->train.ids && g.cap == h->train.cap &&
            g.b0 == h->band0 && g.b1 == h->band1 &&
-           g.bwd == effective_bwd(h) && g.prof == h->prof.on && g.pmask == h->prof.mask;
+           g.bwd == effective_bwd(h) && g.prof == h->prof.on && g.pmask == h->prof.mask &&
+           g.warm == h->skip_records && g.fused == h->fuse_now;
 }
 
 // Capture forward_backward + k_adam(mode) on the private capture stream.
@@ -831,7 +881,7 @@ void capture(smoe_ctx *h, StepGraph &g, int mode, const smoe_params *p, const fl
     CK(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
     try {
         forward_backward(h, p, t);
-        launch_adam(h, mode, p, nullptr, gout, lr);
+        launch_adam(h, mode, p, nullptr, gout, lr, 0, -1, nullptr, h->fuse_now);
     } catch (...) {
         cudaStreamEndCapture(h->cap_stream, &graph);
         if (graph) cudaGraphDestroy(graph);
@@ -878,6 +928,7 @@ void capture(smoe_ctx *h, StepGraph &g, int mode, const smoe_params *p, const fl
     g.target = t; g.gout = gout; g.ids = h->train.ids; g.cap = h->train.cap;
     g.b0 = h->band0; g.b1 = h->band1; g.bwd = effective_bwd(h);
     g.prof = h->prof.on; g.pmask = h->prof.mask;
+    g.warm = h->skip_records; g.fused = h->fuse_now;
     g.valid = true;
 }
 
@@ -885,7 +936,7 @@ void capture(smoe_ctx *h, StepGraph &g, int mode, const smoe_params *p, const fl
 void replay(smoe_ctx *h, StepGraph &g, const smoe_params *p, float *gout, const smoe_lr *lr)
 {
     AdamArgs a;
-    adam_args(h, p, nullptr, gout, lr, a);
+    adam_args(h, p, nullptr, gout, lr, a, 0, -1, nullptr, g.fused);
     cudaKernelNodeParams kp = {};
     kp.func = g.adam_func;
     kp.gridDim = g.adam_grid;
@@ -910,14 +961,28 @@ void replay(smoe_ctx *h, StepGraph &g, const smoe_params *p, float *gout, const 
 
 // One step (mode 0) or gradient pass (mode 1): graph replay once the grid
 // is calibrated, eager launches otherwise.
+struct SeqFlags {
+    smoe_ctx *h;
+    ~SeqFlags() { h->skip_records = h->fuse_now = false; }
+};
+
 void run_sequence(smoe_ctx *h, int mode, const smoe_params *p, const float *t, float *gout, const smoe_lr *lr)
 {
+    // fused records: skip k_records when the previous step's Adam wrote them
+    // for these parameters; this step's Adam (mode 0) writes the next ones
+    const bool fuse = fuse_rec(h);
+    SeqFlags flags_{h};
+    h->skip_records = fuse && rec_is_fresh(h, p);
+    h->fuse_now = fuse && mode == 0;
+    invalidate_rec(h);
     bool ready = h->use_graphs && h->train.calibrated && h->train.oH == h->H && h->train.oW == h->W &&
                  h->train.cnt != nullptr;
     if (!ready) {
         forward_backward(h, p, t);
-        launch_adam(h, mode, p, nullptr, gout, lr);
+        launch_adam(h, mode, p, nullptr, gout, lr, 0, -1, nullptr, h->fuse_now);
         release_target(h);
+        // mode 1 leaves the parameters (and the records just used) as they were
+        if (fuse) mark_rec_fresh(h, p);
         return;
     }
     // graph cache lookup (key: buffers, band, modes); evict the least recent
@@ -933,6 +998,7 @@ void run_sequence(smoe_ctx *h, int mode, const smoe_params *p, const float *t, f
     h->sg_use[mode][hit] = ++h->sg_clock;
     replay(h, h->sg[mode][hit], p, gout, lr);
     release_target(h);
+    if (fuse) mark_rec_fresh(h, p);
 }
 
 }  // namespace
@@ -1105,6 +1171,13 @@ smoe_status smoe_set_band(smoe_handle h, int r0, int r1)
     return SMOE_OK;
 }
 
+smoe_status smoe_invalidate(smoe_handle h)
+{
+    if (!h) return SMOE_ERR_BAD_HANDLE;
+    h->rec_fresh = false;
+    return SMOE_OK;
+}
+
 smoe_status smoe_reset_adam(smoe_handle h)
 {
     if (!h) return SMOE_ERR_BAD_HANDLE;
@@ -1210,6 +1283,7 @@ smoe_status smoe_apply_ex(smoe_handle h, smoe_params *p, const float *grad, cons
             }
         }
         if (k1 == k0) return SMOE_OK;
+        invalidate_rec(h);   // parameters change outside a step
         const float *g = grad;
         size_t n = (size_t)(k1 - k0) * h->P;
         if (!is_device_ptr(grad)) {
@@ -1240,6 +1314,7 @@ smoe_status smoe_render_ex(smoe_handle h, const smoe_params *p, int out_H, int o
         if (!(sharpen > 0.0f && sharpen <= 1.0f))
             throw SmoeError(SMOE_ERR_INVALID_ARG, "smoe_render: sharpen must be in (0, 1]");
         float lscale = sqrtf(sharpen);
+        invalidate_rec(h);   // the render binning overwrites the records and tile boxes
         refresh_perm(h, p, false);
         h->perm_age++;
         bool odev = is_device_ptr(out);

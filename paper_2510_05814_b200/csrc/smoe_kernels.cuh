@@ -254,6 +254,74 @@ __device__ __forceinline__ bool block_meets(float mux, float muy, float a, float
 // block rows [ty_lo, ty_hi) (the whole grid, or one multi-GPU band).
 // Whitening: u = a dx, v = b dx + c dy with a = 1/l11, b = -l21/(l11 l22),
 // c = 1/l22, so d^2 = u^2 + v^2 = delta^T Sigma^-1 delta.
+// Record (whitening, log2 pi, experts) and tile box of one kernel from its
+// parameter values; shared by the binning kernels and the fused Adam epilogue
+// (which writes the next step's records from the parameters it just
+// updated).  Returns the inclusive block box {x0, x1, y0, y1} of the raster,
+// or -1s when the kernel covers no pixel centre or a value is not finite.
+template <int C, int E>
+__device__ __forceinline__ int4 record_box(float2 mu, float l11, float l21, float l22, float lp, const float *ex,
+                                           float R2, float sx, float sy, int oW, int oH, int mode,
+                                           float (&r)[Rec<C, E>::RS], bool &ok)
+{
+    using R = Rec<C, E>;
+    float a = 1.0f / l11, c = 1.0f / l22;
+    float b = -l21 / (l11 * l22);
+    r[0] = mu.x; r[1] = mu.y; r[2] = a; r[3] = b; r[4] = c; r[5] = lp * LOG2E;
+    ok = finitef(mu.x) && finitef(mu.y) && finitef(a) && finitef(b) && finitef(c) && finitef(lp);
+#pragma unroll
+    for (int i = 0; i < C * E; i++) {
+        r[6 + i] = ex[i];
+        ok = ok && finitef(r[6 + i]);
+    }
+#pragma unroll
+    for (int i = R::P; i < R::RS; i++) r[i] = 0.0f;
+    float s11 = l11 * l11, s12 = l11 * l21, s22 = l21 * l21 + l22 * l22;
+    float rx, ry;
+    if (mode == 0) {
+        float h = 0.5f * (s11 - s22);
+        float lmax = 0.5f * (s11 + s22) + sqrtf(h * h + s12 * s12);
+        rx = ry = sqrtf(R2 * lmax);
+    } else {
+        rx = sqrtf(R2 * s11);
+        ry = sqrtf(R2 * s22);
+    }
+    float xl = ceilf((mu.x - rx + 0.5f) * sx - 0.5f);
+    float xh = floorf((mu.x + rx + 0.5f) * sx - 0.5f);
+    float yl = ceilf((mu.y - ry + 0.5f) * sy - 0.5f);
+    float yh = floorf((mu.y + ry + 0.5f) * sy - 0.5f);
+    xl = fmaxf(xl, 0.0f); yl = fmaxf(yl, 0.0f);
+    xh = fminf(xh, (float)(oW - 1)); yh = fminf(yh, (float)(oH - 1));
+    if (ok && xl <= xh && yl <= yh) return make_int4((int)xl / TILE, (int)xh / TILE, (int)yl / TILE, (int)yh / TILE);
+    return make_int4(-1, -1, -1, -1);
+}
+
+// Destination of the fused Adam epilogue's records (training grid, current
+// band, lscale 1); rec == nullptr: no records (standalone binning follows).
+struct RecOut {
+    float *rec;
+    int4 *tbox;
+    float R2;
+    int oW, oH, ty_lo, ty_hi, mode;
+};
+
+template <int C, int E>
+__device__ __forceinline__ void write_record(const RecOut &ro, int k, float2 mu, float l11, float l21, float l22,
+                                             float lp, const float *ex, HandleCtr *hc)
+{
+    using R = Rec<C, E>;
+    float r[R::RS];
+    bool ok;
+    const int4 tb = record_box<C, E>(mu, l11, l21, l22, lp, ex, ro.R2, 1.0f, 1.0f, ro.oW, ro.oH, ro.mode, r, ok);
+    if (!ok) atomicExch((unsigned long long *)&hc->nonfinite, 1ull);
+    if (tb.x >= 0 && max(tb.z, ro.ty_lo) <= min(tb.w, ro.ty_hi - 1)) {
+        float4 *dst = reinterpret_cast<float4 *>(ro.rec) + (size_t)k * (R::RS / 4);
+#pragma unroll
+        for (int q = 0; q < R::RS / 4; q++) dst[q] = make_float4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+    }
+    ro.tbox[k] = tb;
+}
+
 template <int C, int E>
 __device__ __forceinline__ void
 preprocess_one(int k, ParamsDev p, float R2, float sx, float sy, int oW, int oH,
@@ -270,40 +338,13 @@ preprocess_one(int k, ParamsDev p, float R2, float sx, float sy, int oW, int oH,
     // lscale = sqrt(s) applies the sharpening edit Sigma -> s Sigma (render only)
     float l11 = p.chol[3 * k] * lscale, l21 = p.chol[3 * k + 1] * lscale, l22 = p.chol[3 * k + 2] * lscale;
     float lp = p.log_pi[k];
-    float a = 1.0f / l11, c = 1.0f / l22;
-    float b = -l21 / (l11 * l22);
     float r[R::RS];
-    r[0] = mu.x; r[1] = mu.y; r[2] = a; r[3] = b; r[4] = c; r[5] = lp * LOG2E;
-    bool ok = finitef(mu.x) && finitef(mu.y) && finitef(a) && finitef(b) && finitef(c) && finitef(lp);
-#pragma unroll
-    for (int i = 0; i < C * E; i++) {
-        r[6 + i] = p.expert[(size_t)k * C * E + i];
-        ok = ok && finitef(r[6 + i]);
-    }
-#pragma unroll
-    for (int i = R::P; i < R::RS; i++) r[i] = 0.0f;
+    bool ok;
+    const int4 tb = record_box<C, E>(mu, l11, l21, l22, lp, p.expert + (size_t)k * C * E, R2, sx, sy, oW, oH, mode, r, ok);
     if (!ok && sub == 0) atomicExch((unsigned long long *)&hc->nonfinite, 1ull);
-
-    float s11 = l11 * l11, s12 = l11 * l21, s22 = l21 * l21 + l22 * l22;
-    float rx, ry;
-    if (mode == 0) {
-        float h = 0.5f * (s11 - s22);
-        float lmax = 0.5f * (s11 + s22) + sqrtf(h * h + s12 * s12);
-        rx = ry = sqrtf(R2 * lmax);
-    } else {
-        rx = sqrtf(R2 * s11);
-        ry = sqrtf(R2 * s22);
-    }
-    float xl = ceilf((mu.x - rx + 0.5f) * sx - 0.5f);
-    float xh = floorf((mu.x + rx + 0.5f) * sx - 0.5f);
-    float yl = ceilf((mu.y - ry + 0.5f) * sy - 0.5f);
-    float yh = floorf((mu.y + ry + 0.5f) * sy - 0.5f);
+    const float a = r[2], b = r[3], c = r[4];
     const BoxGeo G{mode, 1.0f / sx, 1.0f / sy, oW, oH};
-    xl = fmaxf(xl, 0.0f); yl = fmaxf(yl, 0.0f);
-    xh = fminf(xh, (float)(oW - 1)); yh = fminf(yh, (float)(oH - 1));
-    int4 tb = make_int4(-1, -1, -1, -1);
-    if (ok && xl <= xh && yl <= yh) {
-        tb = make_int4((int)xl / TILE, (int)xh / TILE, (int)yl / TILE, (int)yh / TILE);
+    if (tb.x >= 0) {
         int y0 = max(tb.z, ty_lo), y1 = min(tb.w, ty_hi - 1);
         // the record is read only through the block lists: write it only for
         // a kernel listed in some block of the band (a multi-GPU rank skips
@@ -626,11 +667,13 @@ k_emit(int K, const int *__restrict__ perm, const int4 *__restrict__ tbox, int n
         const int area = wcols * wrows;
         for (int w = tid; w < area; w += EMIT_NT) s_cnt[w] = 0;
         __syncthreads();
-        for (int e = 0; e < nbx; e++) {
-            const int yy = tb.z + e / wx, xx = tb.x + e % wx;
-            if (!rec_meets(rec, rs4, k, xx, yy, G, R2)) continue;
-            atomicAdd(&s_cnt[(yy - mny) * wcols + (xx - mnx)], 1);
-            n_emit++;
+        for (int yy = tb.z; yy <= tb.w; yy++) {
+            const int wrow = (yy - mny) * wcols - mnx;
+            for (int xx = tb.x; xx <= tb.y; xx++) {
+                if (!rec_meets(rec, rs4, k, xx, yy, G, R2)) continue;
+                atomicAdd(&s_cnt[wrow + xx], 1);
+                n_emit++;
+            }
         }
         __syncthreads();
         // one returning global atomic per window block that has entries
@@ -645,24 +688,27 @@ k_emit(int K, const int *__restrict__ perm, const int4 *__restrict__ tbox, int n
             }
         }
         __syncthreads();
-        for (int e = 0; e < nbx; e++) {
-            const int yy = tb.z + e / wx, xx = tb.x + e % wx;
-            if (!rec_meets(rec, rs4, k, xx, yy, G, R2)) continue;
-            const int w = (yy - mny) * wcols + (xx - mnx);
-            const int sl = s_base[w] + atomicAdd(&s_cnt[w], 1);
-            if (sl < bcap) dids[(size_t)(yy * nx + xx) * bcap + sl] = k;
+        for (int yy = tb.z; yy <= tb.w; yy++) {
+            const int wrow = (yy - mny) * wcols - mnx;
+            for (int xx = tb.x; xx <= tb.y; xx++) {
+                if (!rec_meets(rec, rs4, k, xx, yy, G, R2)) continue;
+                const int w = wrow + xx;
+                const int sl = s_base[w] + atomicAdd(&s_cnt[w], 1);
+                if (sl < bcap) dids[(size_t)(yy * nx + xx) * bcap + sl] = k;
+            }
         }
     } else {
         // window too large (huge or scattered kernels): per-entry atomics
+        int yy = tb.z, xx = tb.x;
         for (int e0 = 0; e0 < nbx; e0 += PRE_ATOM) {
             int t[PRE_ATOM], sl[PRE_ATOM];
             bool on[PRE_ATOM];
 #pragma unroll
             for (int q = 0; q < PRE_ATOM; q++) {
-                const int e = e0 + q, yy = tb.z + e / wx, xx = tb.x + e % wx;
                 t[q] = yy * nx + xx;
-                on[q] = e < nbx && rec_meets(rec, rs4, k, xx, yy, G, R2);
+                on[q] = e0 + q < nbx && rec_meets(rec, rs4, k, xx, yy, G, R2);
                 sl[q] = on[q] ? atomicAdd(&cnt[t[q]], 1) : bcap;
+                if (++xx > tb.y) { xx = tb.x; yy++; }
             }
 #pragma unroll
             for (int q = 0; q < PRE_ATOM; q++) {
@@ -1645,12 +1691,17 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
                 }
             };
             auto flush = [&] {
+                // unpacked sums live in .x alone (.y stays +0): no x + 0 adds
+                constexpr bool PEf = (SMOE_BWD_PACK & 1) != 0, PGf = (SMOE_BWD_PACK & 2) != 0;
 #pragma unroll
                 for (int q4 = 0; q4 < (R::P + 3) / 4; q4++) {
                     float t4[4];
 #pragma unroll
-                    for (int k4 = 0; k4 < 4; k4++)
-                        t4[k4] = (4 * q4 + k4 < R::P) ? A2[4 * q4 + k4].x + A2[4 * q4 + k4].y : 0.f;
+                    for (int k4 = 0; k4 < 4; k4++) {
+                        const int i = 4 * q4 + k4;
+                        const bool packed = i < 6 ? PGf : PEf;
+                        t4[k4] = i < R::P ? (packed ? A2[i].x + A2[i].y : A2[i].x) : 0.f;
+                    }
                     atomicAdd(dst + q4, make_float4(t4[0], t4[1], t4[2], t4[3]));
                 }
             };
@@ -2011,7 +2062,7 @@ template <int C, int E, int MODE>
 __global__ void __launch_bounds__(ADAM_NT)
 k_adam(AdamCommon cm, ParamsMut p, float *__restrict__ acc, const float *__restrict__ grad_in,
        float *__restrict__ grad_out, float *__restrict__ m1, float *__restrict__ m2,
-       LrDev lr, HandleCtr *hc, const GridCtr *gc, long long cap)
+       LrDev lr, HandleCtr *hc, const GridCtr *gc, long long cap, RecOut ro)
 {
     using R = Rec<C, E>;
     constexpr int P = R::P, V = R::V, KPB = ADAM_NT / V, KPC = ADAM_IT * KPB;
@@ -2044,7 +2095,7 @@ k_adam(AdamCommon cm, ParamsMut p, float *__restrict__ acc, const float *__restr
             if (live && MODE != 1) { a1[it] = m1[(size_t)v * K + k]; a2[it] = m2[(size_t)v * K + k]; }
             if (live && MODE == 2) gi[it] = grad_in[(size_t)(k - k0r) * P + v];
         }
-        float rv[ADAM_IT], pv[ADAM_IT];
+        float rv[ADAM_IT], pv[ADAM_IT], xs[ADAM_IT];
 #pragma unroll
         for (int it = 0; it < ADAM_IT; it++) {
             const int kl = it * KPB + (int)threadIdx.x / V, v = threadIdx.x % V, k = k0 + kl;
@@ -2110,9 +2161,25 @@ k_adam(AdamCommon cm, ParamsMut p, float *__restrict__ acc, const float *__restr
                 m1[(size_t)v * K + k] = n1;
                 m2[(size_t)v * K + k] = n2;
                 *param_slot<C, E>(p, k, v) = x;
+                xs[it] = x;
             }
         }
         __syncthreads();   // shared staging is reused by the next chunk
+        if (MODE != 1 && ro.rec) {
+            // fused epilogue: the next step's records and tile boxes (stage 1
+            // of the two-stage binning) from the parameters just written
+#pragma unroll
+            for (int it = 0; it < ADAM_IT; it++) {
+                const int kl = it * KPB + threadIdx.x % KPB, k = k0 + kl;
+                if (v < P && k < kend) s_prm[kl][v] = xs[it];
+            }
+            __syncthreads();
+            if ((int)threadIdx.x < KPC && k0 + (int)threadIdx.x < kend) {
+                const float *q = s_prm[threadIdx.x];
+                write_record<C, E>(ro, k0 + threadIdx.x, make_float2(q[0], q[1]), q[2], q[3], q[4], q[5], q + 6, hc);
+            }
+            __syncthreads();
+        }
     }
     if (bad) atomicExch((unsigned long long *)&hc->nonfinite, 1ull);
     if (MODE == 1) return;
@@ -2133,7 +2200,7 @@ template <int C, int E, int MODE>
 __global__ void __launch_bounds__(64)
 k_adam_kt(AdamCommon cm, ParamsMut p, float *__restrict__ acc, const float *__restrict__ grad_in,
        float *__restrict__ grad_out, float *__restrict__ m1, float *__restrict__ m2,
-       LrDev lr, HandleCtr *hc, const GridCtr *gc, long long cap)
+       LrDev lr, HandleCtr *hc, const GridCtr *gc, long long cap, RecOut ro)
 {
     using R = Rec<C, E>;
     constexpr int P = R::P;
@@ -2223,6 +2290,9 @@ k_adam_kt(AdamCommon cm, ParamsMut p, float *__restrict__ acc, const float *__re
             p.log_pi[k] = prm[5];
 #pragma unroll
             for (int i = 6; i < P; i++) p.expert[(size_t)k * C * E + (i - 6)] = prm[i];
+            // fused epilogue: the next step's record and tile box (stage 1 of
+            // the two-stage binning) from the parameters just written
+            if (ro.rec) write_record<C, E>(ro, k, make_float2(prm[0], prm[1]), prm[2], prm[3], prm[4], prm[5], prm + 6, hc);
         }
     }
     if (MODE == 1) return;

@@ -96,6 +96,7 @@ def lib():
         "smoe_render_ex": (st, [H, ctypes.POINTER(c_params), I, I, P, ctypes.POINTER(c_render_options)]),
         "smoe_step": (st, [H, ctypes.POINTER(c_params), P, ctypes.POINTER(c_lr), ctypes.POINTER(c_stats)]),
         "smoe_set_band": (st, [H, I, I]),
+        "smoe_invalidate": (st, [H]),
         "smoe_grad": (st, [H, ctypes.POINTER(c_params), P, P, P]),
         "smoe_apply": (st, [H, ctypes.POINTER(c_params), P, ctypes.POINTER(c_lr)]),
         "smoe_apply_ex": (st, [H, ctypes.POINTER(c_params), P, ctypes.POINTER(c_lr), I, I, P]),
@@ -280,6 +281,15 @@ class SMoE:
     def _p(self, params: Params) -> c_params:
         return params.c(self.K, self.C, self.E, self.device)
 
+    def _fresh(self, params: Params):
+        """Fused records (smoe_invalidate): tell the library when the caller
+        wrote the parameter tensors since the last step (their version
+        counters moved; the library's own writes do not move them)."""
+        key = tuple((t.data_ptr(), t._version) for t in (params.mu, params.chol, params.log_pi, params.expert))
+        if key != getattr(self, "_pkey", None):
+            _check(lib().smoe_invalidate(self.h), self.h)
+        self._pkey = key
+
     def _target(self, target):
         return _ptr(target, "target", torch.float32, self.C * self.H * self.W, self.device)
 
@@ -290,6 +300,7 @@ class SMoE:
         lr = lr or LR()
         p = self._p(params)
         t = self._target(target)
+        self._fresh(params)
         if stats:
             s = c_stats()
             _check(lib().smoe_step(self.h, ctypes.byref(p), t, ctypes.byref(lr.c()), ctypes.byref(s)), self.h)
@@ -336,6 +347,7 @@ class SMoE:
             grad = torch.empty((self.K, self.Pk), dtype=torch.float32, device=dev)
         if sums is None:
             sums = torch.empty(4, dtype=torch.float64, device=dev)
+        self._fresh(params)
         _check(lib().smoe_grad(self.h, ctypes.byref(self._p(params)), self._target(target),
                                _ptr(grad, "grad", torch.float32, self.K * self.Pk, self.device),
                                _ptr(sums, "sums", torch.float64, 4, self.device)), self.h)
