@@ -1,4 +1,4 @@
-"""Fused records (include/smoe.h smoe_invalidate; DESIGN.md §5): with the
+"""Fused records (include/smoe.h smoe_invalidate; DESIGN.md §3): with the
 two-stage binning the Adam of smoe_step writes the next step's kernel
 records and tile boxes (the geometry of P:215-221) for the parameters it
 just updated, and the next step on the same parameters skips k_records.
@@ -30,10 +30,17 @@ def _grad(h, prm, tgt):
     return g.cpu().numpy().astype(np.float64), s.cpu().numpy()
 
 
+# binning -> (SMOE_PERM, launches of a warm step, of a cold step); one-pass
+# binning (SMOE_PERM=0 at this K) has no fused form: every step is cold
+BINNINGS = {"two_stage": ("1", 3, 4), "one_pass": ("0", 3, 3)}
+
+
+@pytest.mark.parametrize("binning", list(BINNINGS))
 @pytest.mark.parametrize("C,order", [(3, 0), (1, 1)])
 @pytest.mark.parametrize("event", [None, "edit", "render", "apply", "band"])
-def test_fused_records_match_fresh_binning(monkeypatch, C, order, event):
-    monkeypatch.setenv("SMOE_PERM", "1")                     # two-stage binning at this small K
+def test_fused_records_match_fresh_binning(monkeypatch, binning, C, order, event):
+    perm, warm, cold = BINNINGS[binning]
+    monkeypatch.setenv("SMOE_PERM", perm)                    # two-stage binning even at this small K, or not
     monkeypatch.setenv("SMOE_FUSE_REC", "1")
     pool = synth.aniso_pool(H, W, C, K, 3, order=order)
     prm = smoe.Params.from_numpy(pool, "cuda:0")
@@ -45,8 +52,8 @@ def test_fused_records_match_fresh_binning(monkeypatch, C, order, event):
         h.step(prm, tgt, smoe.LR(), stats=(it == 0))
         torch.cuda.synchronize()
         launches.append(h.launch_count() - n0)
-    # steady state: k_emit, raster, Adam (the Adam wrote the records)
-    assert launches[3:] == [3, 3, 3], launches
+    # steady state: (k_emit,) raster, Adam (the Adam wrote the records)
+    assert launches[3:] == [warm] * 3, launches
     band = None
     if event == "edit":
         prm.mu.add_(0.37)                                    # the caller writes the parameters
@@ -60,8 +67,8 @@ def test_fused_records_match_fresh_binning(monkeypatch, C, order, event):
         h.set_band(*band)
     n0 = h.launch_count()
     g1, s1 = _grad(h, prm, tgt)
-    # warm (2 launches + Adam chain rule) only when nothing invalidated
-    assert h.launch_count() - n0 == (3 if event is None else 4)
+    # warm only when nothing invalidated
+    assert h.launch_count() - n0 == (warm if event is None else cold)
     h2 = smoe.SMoE(K, H, W, C, order)
     if band:
         h2.set_band(*band)
@@ -75,9 +82,11 @@ def test_fused_records_match_fresh_binning(monkeypatch, C, order, event):
     assert not bad.any(), f"{bad.sum()} gradient entries differ, worst {np.abs(g1 - g2).max():.3e}"
 
 
-def test_fused_records_off_launches_k_records(monkeypatch):
-    """SMOE_FUSE_REC=0: every step runs k_records (4 launches)."""
-    monkeypatch.setenv("SMOE_PERM", "1")
+@pytest.mark.parametrize("binning", list(BINNINGS))
+def test_fused_records_off_launches_k_records(monkeypatch, binning):
+    """SMOE_FUSE_REC=0: every step runs its own preprocessing."""
+    perm, warm, cold = BINNINGS[binning]
+    monkeypatch.setenv("SMOE_PERM", perm)
     monkeypatch.setenv("SMOE_FUSE_REC", "0")
     C, order = 3, 0
     pool = synth.aniso_pool(H, W, C, K, 3, order=order)
@@ -91,4 +100,34 @@ def test_fused_records_off_launches_k_records(monkeypatch):
         torch.cuda.synchronize()
         launches.append(h.launch_count() - n0)
     h.close()
-    assert launches[2:] == [4, 4, 4], launches
+    assert launches[2:] == [cold] * 3, launches
+
+
+@pytest.mark.parametrize("binning", list(BINNINGS))
+def test_fused_emission_overflow_recovers(monkeypatch, binning):
+    """A step whose update grows the kernels past the bucket capacity: the
+    next step's binning (on fused or fresh records) overflows, is skipped,
+    grown and redone; the trajectory must match the unfused one."""
+    perm = BINNINGS[binning][0]
+    monkeypatch.setenv("SMOE_PERM", perm)
+    C, order = 3, 0
+    pool = synth.aniso_pool(H, W, C, K, 5, order=order)
+    tgt = torch.as_tensor(synth.image(H, W, C, 6)).cuda()
+    big = smoe.LR(mu=0.01, chol=1.5, log_pi=0.01, expert=0.01, slope=0.0)   # Cholesky factors jump by ~1.5 px
+    runs = []
+    for fuse in ("0", "1"):
+        monkeypatch.setenv("SMOE_FUSE_REC", fuse)
+        prm = smoe.Params.from_numpy(pool, "cuda:0")
+        h = smoe.SMoE(K, H, W, C, order)
+        losses, pairs = [], []
+        for it in range(10):
+            st = h.step(prm, tgt, big if it == 4 else smoe.LR())
+            losses.append(st.loss)
+            pairs.append(st.pairs)
+        runs.append(([t.cpu().numpy().astype(np.float64) for t in (prm.mu, prm.chol, prm.log_pi, prm.expert)],
+                     np.array(losses)))
+        h.close()
+    (pa, la), (pb, lb) = runs
+    np.testing.assert_allclose(lb, la, rtol=1e-4)
+    for x, y in zip(pa, pb):
+        np.testing.assert_allclose(y, x, rtol=1e-3, atol=1e-4)
