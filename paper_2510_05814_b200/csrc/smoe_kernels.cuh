@@ -2196,8 +2196,13 @@ k_adam(AdamCommon cm, ParamsMut p, float *__restrict__ acc, const float *__restr
 // Large pools: one thread per kernel, all of its loads first (more bytes in
 // flight per thread than the element-parallel form once several waves are
 // needed; measured faster at K >= 20 000).
+#ifndef SMOE_ADAMKT_MINB
+#define SMOE_ADAMKT_MINB 12  // k_adam_kt: min resident 64-thread CTAs per SM (<= 80 registers, no spills;
+                             // config 3 Adam 15.9 -> 13.7 us, config 5 77 -> 70 us against the uncapped
+                             // 106 registers); C = 3 linear experts stay uncapped (they would spill)
+#endif
 template <int C, int E, int MODE>
-__global__ void __launch_bounds__(64)
+__global__ void __launch_bounds__(64, (C == 3 && E == 3) ? 1 : SMOE_ADAMKT_MINB)
 k_adam_kt(AdamCommon cm, ParamsMut p, float *__restrict__ acc, const float *__restrict__ grad_in,
        float *__restrict__ grad_out, float *__restrict__ m1, float *__restrict__ m2,
        LrDev lr, HandleCtr *hc, const GridCtr *gc, long long cap, RecOut ro)
