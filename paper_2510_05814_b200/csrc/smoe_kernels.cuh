@@ -2058,8 +2058,12 @@ __device__ __forceinline__ bool adam_skipped(const AdamCommon &cm, float *grad_o
     return true;
 }
 
+#ifndef SMOE_ADAM_MINB
+#define SMOE_ADAM_MINB 6     // k_adam: min resident CTAs per SM (40 registers: config 2 Adam 11.6 -> 9.5 us,
+                             // step 62.5 -> 60.9 us; config 4 neutral; 8 measured equal)
+#endif
 template <int C, int E, int MODE>
-__global__ void __launch_bounds__(ADAM_NT)
+__global__ void __launch_bounds__(ADAM_NT, SMOE_ADAM_MINB)
 k_adam(AdamCommon cm, ParamsMut p, float *__restrict__ acc, const float *__restrict__ grad_in,
        float *__restrict__ grad_out, float *__restrict__ m1, float *__restrict__ m2,
        LrDev lr, HandleCtr *hc, const GridCtr *gc, long long cap, RecOut ro)
