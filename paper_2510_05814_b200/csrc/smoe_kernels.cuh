@@ -413,8 +413,11 @@ __device__ __forceinline__ void finish_direct(int bcap, GridCtr *gc, double *dst
     }
 }
 
+#ifndef SMOE_PRE_MINB
+#define SMOE_PRE_MINB 1      // k_preprocess: min resident CTAs per SM (register cap; 6 and 8 spill and lose 12-16%)
+#endif
 template <int C, int E>
-__global__ void __launch_bounds__(PRE_NT)
+__global__ void __launch_bounds__(PRE_NT, SMOE_PRE_MINB)
 k_preprocess(int K, ParamsDev p, float R2, float sx /* oW/W */, float sy /* oH/H */, int oW, int oH,
              int nx, int ty_lo, int ty_hi, float *__restrict__ rec,
              int4 *__restrict__ tbox, int *__restrict__ cnt, HandleCtr *hc,
@@ -617,8 +620,11 @@ __device__ __forceinline__ bool rec_meets(const float *rec, int rs4, int k, int 
     return block_meets(f0.x, f0.y, f0.z, f0.w, c, tx, ty, G, R2);
 }
 
+#ifndef SMOE_EMIT_MINB
+#define SMOE_EMIT_MINB 1     // k_emit: min resident CTAs per SM (register cap; 8: config 5 -14%, config 3 +9%)
+#endif
 // stage 2: bucket emission, CTA-aggregated over a shared window of blocks
-__global__ void __launch_bounds__(EMIT_NT)
+__global__ void __launch_bounds__(EMIT_NT, SMOE_EMIT_MINB)
 k_emit(int K, const int *__restrict__ perm, const int4 *__restrict__ tbox, int nx, int ty_lo, int ty_hi,
        int *__restrict__ cnt, int *__restrict__ dids, int bcap, GridCtr *gc, double *dstats,
        const float *__restrict__ rec, int rs4, BoxGeo G, float R2)
@@ -1939,7 +1945,10 @@ __device__ __forceinline__ void render_tile4(const RasterArgs &A, const int tile
 }
 
 template <int C, int E, bool PROF>
-__global__ void __launch_bounds__(R4_NT, 16)
+#ifndef SMOE_R4_MINB
+#define SMOE_R4_MINB 16
+#endif
+__global__ void __launch_bounds__(R4_NT, SMOE_R4_MINB)
 k_render4(RasterArgs A)
 {
     const int tile = A.tile0 + blockIdx.x;
