@@ -545,14 +545,15 @@ def main():
         # fused records: with the two-stage binning the Adam
         # also writes the next step's tile box and record (no k_records launch)
         fused = two and "k_preprocess" not in breakdown
-        adam_bytes = K * (24 * Pk + 8 * V) + (K * (16 + RSb) if fused else 0)
+        Vu = 4 * ((Pk + 3) // 4)                 # raw-sum slots read + zeroed (the used float4 chunks)
+        adam_bytes = K * (24 * Pk + 8 * Vu) + (K * (16 + RSb) if fused else 0)
         for name, b, what in (("k_preprocess", pre_bytes, f"read params {4 * Pk} B + write tile box 16 B + record "
                                                         f"{RSb} B per kernel" + ("" if two else ", + 4 B kernel id per "
                                                         "pair (count atomics are L2 traffic, not counted)")),
                               ("k_emit", emit_bytes, "read the spatial order 4 B + tile box 16 B per kernel, write "
                                                      "4 B kernel id per pair (one count atomic per CTA and block)"),
                               ("k_adam", adam_bytes, f"per kernel: params, m1, m2 read + write ({24 * Pk} B), raw "
-                                                     f"sums read + zeroed ({8 * V} B)" +
+                                                     f"sums read + zeroed ({8 * Vu} B)" +
                                                      (f", next step's tile box + record written ({16 + RSb} B)"
                                                       if fused else ""))):
             if name in breakdown and breakdown[name] > 0:

@@ -2114,7 +2114,7 @@ k_adam(AdamCommon cm, ParamsMut p, float *__restrict__ acc, const float *__restr
             const int kl = it * KPB + (int)threadIdx.x / V, v = threadIdx.x % V, k = k0 + kl;
             rv[it] = pv[it] = 0.f;
             if (k < kend) {
-                if (MODE != 2) rv[it] = acc[(size_t)k0 * V + it * ADAM_NT + threadIdx.x];
+                if (MODE != 2 && v < P) rv[it] = acc[(size_t)k0 * V + it * ADAM_NT + threadIdx.x];
                 pv[it] = *param_slot<C, E>(p, k, min(v, P - 1));
             }
         }
@@ -2128,7 +2128,8 @@ k_adam(AdamCommon cm, ParamsMut p, float *__restrict__ acc, const float *__restr
         if (MODE != 2) {
 #pragma unroll
             for (int it = 0; it < ADAM_IT; it++)
-                if (k0 + it * KPB + (int)threadIdx.x / V < kend) acc[(size_t)k0 * V + it * ADAM_NT + threadIdx.x] = 0.f;
+                if (k0 + it * KPB + (int)threadIdx.x / V < kend && (int)threadIdx.x % V < P)
+                    acc[(size_t)k0 * V + it * ADAM_NT + threadIdx.x] = 0.f;
         }
 #pragma unroll
         for (int it = 0; it < ADAM_IT; it++) {
@@ -2245,9 +2246,11 @@ k_adam_kt(AdamCommon cm, ParamsMut p, float *__restrict__ acc, const float *__re
 #pragma unroll
             for (int i = 0; i < P; i++) g[i] = grad_in[(size_t)kr * P + i];
         } else {
+            // only the float4 chunks holding the P sums (slots >= P are never
+            // written by the raster and stay zero from the allocation)
             const float4 *ap = reinterpret_cast<const float4 *>(acc) + (size_t)k * (R::V / 4);
 #pragma unroll
-            for (int q = 0; q < R::V / 4; q++) {
+            for (int q = 0; q < (P + 3) / 4; q++) {
                 float4 f = ap[q];
                 raw[4 * q] = f.x; raw[4 * q + 1] = f.y; raw[4 * q + 2] = f.z; raw[4 * q + 3] = f.w;
             }
@@ -2278,7 +2281,7 @@ k_adam_kt(AdamCommon cm, ParamsMut p, float *__restrict__ acc, const float *__re
             for (int i = 6; i < P; i++) g[i] = raw[i];
             float4 *ap = reinterpret_cast<float4 *>(acc) + (size_t)k * (R::V / 4);
 #pragma unroll
-            for (int q = 0; q < R::V / 4; q++) ap[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int q = 0; q < (P + 3) / 4; q++) ap[q] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         bool ok = true;
 #pragma unroll
