@@ -16,8 +16,9 @@ that sum, done as
      uncovered, skipped) (fp64, 32 bytes);
   3. Adam on the rank's shard only (``smoe_apply_ex(k0, k1, sums)``; skipped
      on every rank alike when any rank's binning overflowed, sums[3] > 0);
-  4. in-place all-gather of the four parameter arrays, padded to Kpad rows,
-     so every rank holds the identical updated parameters.
+  4. all-gather of the four parameter arrays, padded to Kpad rows (packed
+     into one collective), so every rank holds the identical updated
+     parameters.
 
 Bytes moved equal the all-reduce's (reduce-scatter + all-gather), the Adam
 work per rank is 1/world of the replicated form, and the Adam moments of
@@ -67,10 +68,20 @@ def reduce_scatter_grads(grad_pad: torch.Tensor, shard: torch.Tensor, sums: torc
 
 def allgather_params(arrays, rank: int, world: int, Ks: int, group=None) -> None:
     """Step 4: in-place all-gather of parameter arrays padded to world*Ks
-    rows; rank r contributes rows [r Ks, (r+1) Ks) of each array."""
-    for a in arrays:
-        v = a.view(world, -1)
-        dist.all_gather_into_tensor(a.view(-1), v[rank], group=group)
+    rows; rank r contributes rows [r Ks, (r+1) Ks) of each array.  ONE
+    collective: the rank's shard rows of every array are packed side by side
+    into a [Ks, W] send buffer (W = the arrays' row widths summed: 6 + C E),
+    gathered into [world, Ks, W] and unpacked (one collective launch and
+    latency instead of four; the bytes are the same)."""
+    views = [a.view(world, Ks, -1) for a in arrays]
+    widths = [v.shape[2] for v in views]
+    send = torch.cat([v[rank] for v in views], dim=1)
+    recv = torch.empty((world,) + tuple(send.shape), dtype=send.dtype, device=send.device)
+    dist.all_gather_into_tensor(recv.view(-1), send.view(-1), group=group)
+    off = 0
+    for v, w in zip(views, widths):
+        v.copy_(recv[:, :, off:off + w])
+        off += w
 
 
 def padded(params, world: int):
