@@ -687,6 +687,7 @@ void forward_backward(smoe_ctx *h, const smoe_params *p, const float *target)
     int nt = (ty_hi - ty_lo) * g.nx;
     if (nt <= 0) return;
     RasterArgs A{};
+    A.K = h->K;
     A.rec = h->rec; A.ids = g.ids; A.tmp = g.tmp; A.start = g.start; A.gc = g.gc; A.cap = g.cap;
     A.len = g.direct ? g.cnt : nullptr; A.lenout = g.len; A.bcap = g.bcap;
     A.order = g.order_valid ? g.order : nullptr;
@@ -748,7 +749,7 @@ RecOut rec_out(smoe_ctx *h)
 {
     int ty_lo, ty_hi;
     band_rows(h, ty_lo, ty_hi);
-    return RecOut{h->rec, h->tbox, h->R2, h->W, h->H, ty_lo, ty_hi, h->box_mode};
+    return RecOut{h->rec, h->tbox, h->R2, h->W, h->H, ty_lo, ty_hi, h->box_mode, h->K};
 }
 
 bool rec_is_fresh(const smoe_ctx *h, const smoe_params *p)
@@ -1327,6 +1328,7 @@ smoe_status smoe_render_ex(smoe_handle h, const smoe_params *p, int out_H, int o
             size_t n = (size_t)h->C * out_H * out_W;
             float *o = odev ? out : stage(h->stage_out, h->stage_out_n, n);
             RasterArgs A{};
+            A.K = h->K;
             A.rec = h->rec; A.ids = g.ids; A.tmp = g.tmp; A.start = g.start; A.gc = g.gc; A.cap = g.cap;
             A.len = g.direct ? g.cnt : nullptr; A.lenout = g.len; A.bcap = g.bcap;
             A.order = g.order_valid ? g.order : nullptr; A.gcw = g.gc; A.n_work = g.n_tiles; A.n_sm = h->n_sm;

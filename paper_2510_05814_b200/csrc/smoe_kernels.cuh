@@ -22,6 +22,7 @@
 #include <stdint.h>
 #include <limits.h>
 #include <type_traits>
+#include <cstdio>
 
 namespace smoe {
 
@@ -45,6 +46,23 @@ constexpr int TILE = 16;                 // 16x16 blocks
 #ifndef SMOE_FWD_PREFETCH
 #define SMOE_FWD_PREFETCH 0              // forward: load record j+1's test half while testing record j
                                          // (measured: +2 registers cost a resident CTA, -9% config 3)
+#endif
+// Device bounds checks of the debug build (-DSMOE_DEBUG; `make variant
+// NAME=dbg EXTRA=-DSMOE_DEBUG`): a failed check prints its site and traps,
+// so the calling test fails with a CUDA error.  Used in place of
+// compute-sanitizer where the tool is unavailable.
+#ifdef SMOE_DEBUG
+#define SMOE_CHECK(c)                                                                    \
+    do {                                                                                 \
+        if (!(c)) {                                                                      \
+            printf("SMOE_CHECK failed at %s:%d: %s\n", __FILE__, __LINE__, #c);          \
+            __trap();                                                                    \
+        }                                                                                \
+    } while (0)
+#else
+#define SMOE_CHECK(c) \
+    do {              \
+    } while (0)
 #endif
 #ifndef SMOE_BWD_PACK
 #define SMOE_BWD_PACK 0                  // kernel-parallel backward: raw sums kept as f32x2 pixel-pair
@@ -303,6 +321,7 @@ struct RecOut {
     int4 *tbox;
     float R2;
     int oW, oH, ty_lo, ty_hi, mode;
+    int K;   // pool size (debug bounds checks)
 };
 
 template <int C, int E>
@@ -319,6 +338,7 @@ __device__ __forceinline__ void write_record(const RecOut &ro, int k, float2 mu,
 #pragma unroll
         for (int q = 0; q < R::RS / 4; q++) dst[q] = make_float4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
     }
+    SMOE_CHECK(k >= 0 && k < ro.K);
     ro.tbox[k] = tb;
 }
 
@@ -371,6 +391,7 @@ preprocess_one(int k, ParamsDev p, float R2, float sx, float sy, int oW, int oH,
                 }
 #pragma unroll
                 for (int q = 0; q < PRE_ATOM; q++) {
+                    SMOE_CHECK(!on[q] || (t[q] >= ty_lo * nx && t[q] < ty_hi * nx));
                     if (sl[q] < bcap) dids[(size_t)t[q] * bcap + sl[q]] = k;
                     if (on[q]) { *max_len = max(*max_len, sl[q] + 1); emitted++; }
                 }
@@ -638,6 +659,7 @@ k_emit(int K, const int *__restrict__ perm, const int4 *__restrict__ tbox, int n
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int i = blockIdx.x * EMIT_NT + tid;
     const int k = i < K ? __ldg(perm + i) : -1;
+    SMOE_CHECK(k < K && (k >= 0 || i >= K));
     int4 tb = make_int4(0, -1, 0, -1);              // empty box
     if (k >= 0) {
         tb = tbox[k];
@@ -700,6 +722,7 @@ k_emit(int K, const int *__restrict__ perm, const int4 *__restrict__ tbox, int n
                 if (!rec_meets(rec, rs4, k, xx, yy, G, R2)) continue;
                 const int w = wrow + xx;
                 const int sl = s_base[w] + atomicAdd(&s_cnt[w], 1);
+                SMOE_CHECK(w >= 0 && w < EMIT_WIN && yy >= ty_lo && yy < ty_hi && xx >= 0 && xx < nx);
                 if (sl < bcap) dids[(size_t)(yy * nx + xx) * bcap + sl] = k;
             }
         }
@@ -1205,6 +1228,7 @@ struct RasterArgs {
     int *len;             // direct buckets (len != null): block t = ids[t bcap, t bcap + len[t]);
                           // len = the binning's count array, reset by the block's CTA
     int *lenout;          // direct buckets: copy of len for the diagnostics (smoe_bin)
+    int K;                // pool size (debug bounds checks)
     int bcap;
     const GridCtr *gc;
     long long cap;
@@ -1340,6 +1364,7 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
         for (int i = threadIdx.x; i < nb * RS4; i += blockDim.x) {
             int j = i / RS4, q = i - j * RS4;
             int id = A.ids[s0 + b0 + j];
+            SMOE_CHECK(id >= 0 && id < A.K && (A.len ? b0 + j < A.bcap : s0 + b0 + j < A.cap));
             srec[i] = reinterpret_cast<const float4 *>(A.rec)[(size_t)id * RS4 + q];
             if (TRAIN && q == 0) sid[j] = id;
         }
@@ -1870,6 +1895,7 @@ __device__ __forceinline__ void render_tile4(const RasterArgs &A, const int tile
         __syncthreads();
         for (int i = threadIdx.x; i < nb * RS4; i += blockDim.x) {
             const int j = i / RS4, q = i - j * RS4;
+            SMOE_CHECK(A.ids[s0 + b0 + j] >= 0 && A.ids[s0 + b0 + j] < A.K && (!A.len || b0 + j < A.bcap));
             srec[i] = reinterpret_cast<const float4 *>(A.rec)[(size_t)A.ids[s0 + b0 + j] * RS4 + q];
         }
         __syncthreads();

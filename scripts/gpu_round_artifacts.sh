@@ -30,7 +30,11 @@ echo mm done
 fi
 if [ $PHASE = b ] || [ $PHASE = all ]; then
 export PYTHONFAULTHANDLER=1
-for tool in memcheck racecheck synccheck initcheck; do
+# device bounds checks of the -DSMOE_DEBUG build (in place of compute-sanitizer where the pool closed it)
+make -s -C paper_2510_05814_b200/csrc variant NAME=dbg EXTRA=-DSMOE_DEBUG
+SMOE_LIB=$PWD/paper_2510_05814_b200/libsmoe_dbg.so timeout 1800 python -m pytest tests -m gpu -q > $O/${TAG}_pytest_gpu_debug_checks.log 2>&1
+echo debug_checks=$?; tail -1 $O/${TAG}_pytest_gpu_debug_checks.log
+for tool in ${SANITIZER_TOOLS:-}; do
 timeout 1500 compute-sanitizer --tool $tool --print-limit 50 --error-exitcode 7 python -m pytest tests/test_gpu_parity.py tests/test_gpu_adam.py tests/test_gpu_fused_records.py -q -x \
    -k "test_grad_parity and 37 or test_render_parity and 37 or binning_large_bucket or dense_buckets or degenerate or step_matches or bucket_over or all_binners or overflow or skips_when or sharded_apply and 300 or fused_records_match and two_stage and 3-0" > $O/${TAG}_sanitizer_$tool.txt 2>&1
 echo $tool=$?; tail -2 $O/${TAG}_sanitizer_$tool.txt
