@@ -64,6 +64,9 @@ constexpr int TILE = 16;                 // 16x16 blocks
     do {              \
     } while (0)
 #endif
+#ifndef SMOE_R4_XF
+#define SMOE_R4_XF 1                     // four-pixel render: cull test on block-centred records (constant experts)
+#endif
 #ifndef SMOE_BWD_PACK
 #define SMOE_BWD_PACK 0                  // kernel-parallel backward: raw sums kept as f32x2 pixel-pair
                                          // accumulators (bit 0: expert sums, bit 1: geometric sums);
@@ -1843,8 +1846,10 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
 // [8w, 8w+8), lane l the vertical strip of four pixels (8w + (l & 7),
 // 4 (l >> 3) + {0..3}).  The four pixels share dx, so per (warp, kernel) the
 // test costs ~23 instructions for 128 pixels (two packed f32x2 pairs in dy)
-// instead of ~34 for two 64-pixel warps of raster_tile.  Same per-pixel
-// arithmetic and list order as raster_tile's render (identical pixels).
+// instead of ~34 for two 64-pixel warps of raster_tile (constant experts:
+// ~20, with the block-centred records of SMOE_R4_XF -- the pixels then
+// agree with raster_tile's render to rounding, both at the oracle bar; the
+// list order, and so the summation order, is the same).
 // Measured: config 3 4x SR +11%, configs 2/5 1x +6%, but config 4 1x (151
 // kernels per block) -7% -- the host picks this form for grids whose
 // longest bucket is short.  The same layout for the TRAIN
@@ -1867,10 +1872,17 @@ __device__ __forceinline__ void render_tile4(const RasterArgs &A, const int tile
     bool vv[4];
 #pragma unroll
     for (int i = 0; i < 4; i++) vv[i] = px < A.oW && py + i < A.oH;
-    // source coordinates of the output samples (Q16)
-    const float xs = (px + 0.5f) * A.sx - 0.5f;
-    const float2 ys01 = make_float2((py + 0.5f) * A.sy - 0.5f, (py + 1.5f) * A.sy - 0.5f);
-    const float2 ys23 = make_float2((py + 2.5f) * A.sy - 0.5f, (py + 3.5f) * A.sy - 0.5f);
+    // source coordinates of the output samples (Q16); XF (constant experts,
+    // SMOE_R4_XF): relative to the block's first sample (X0, Y0), with the
+    // staged records re-centred to {a, -a mx, b, -(b mx + c my), c, ...},
+    // (mx, my) = mu - (X0, Y0), so the cull test is u = a x + alpha,
+    // w = c y + (b x + gamma): 7 instead of 10 FP32 instructions per kernel
+    constexpr bool XF = SMOE_R4_XF && E == 1;
+    const float X0 = XF ? (tx * TILE + 0.5f) * A.sx - 0.5f : 0.f;
+    const float Y0 = XF ? (ty * TILE + 0.5f) * A.sy - 0.5f : 0.f;
+    const float xs = (px + 0.5f) * A.sx - 0.5f - X0;
+    const float2 ys01 = make_float2((py + 0.5f) * A.sy - 0.5f - Y0, (py + 1.5f) * A.sy - 0.5f - Y0);
+    const float2 ys23 = make_float2((py + 2.5f) * A.sy - 0.5f - Y0, (py + 3.5f) * A.sy - 0.5f - Y0);
     const float R2 = A.R2;
     const int s0 = A.len ? tile * A.bcap : A.start[tile];
     const int n = A.len ? A.len[tile] : A.start[tile + 1] - s0;
@@ -1899,6 +1911,15 @@ __device__ __forceinline__ void render_tile4(const RasterArgs &A, const int tile
             srec[i] = reinterpret_cast<const float4 *>(A.rec)[(size_t)A.ids[s0 + b0 + j] * RS4 + q];
         }
         __syncthreads();
+        if (XF) {
+            for (int j = threadIdx.x; j < nb; j += blockDim.x) {
+                const float4 f0 = srec[j * RS4];
+                const float c = srec[j * RS4 + 1].x;
+                const float mx = f0.x - X0, my = f0.y - Y0;
+                srec[j * RS4] = make_float4(f0.z, -f0.z * mx, f0.w, -fmaf(f0.w, mx, c * my));
+            }
+            __syncthreads();
+        }
 #pragma unroll 1
         for (int j = 0; j < nb; j++) {
             float r[R::RS];
@@ -1907,10 +1928,21 @@ __device__ __forceinline__ void render_tile4(const RasterArgs &A, const int tile
                 const float4 f = srec[j * RS4 + q];
                 r[4 * q] = f.x; r[4 * q + 1] = f.y; r[4 * q + 2] = f.z; r[4 * q + 3] = f.w;
             }
-            const float dx = xs - r[0];
-            const float2 dy01 = __fadd2_rn(ys01, make_float2(-r[1], -r[1]));
-            const float2 dy23 = __fadd2_rn(ys23, make_float2(-r[1], -r[1]));
-            const float u = r[2] * dx, bdx = r[3] * dx, uu = u * u;
+            float dx, u, bdx;
+            float2 dy01, dy23;
+            if (XF) {
+                dx = 0.f; dy01 = dy23 = make_float2(0.f, 0.f);   // unused (constant experts)
+                u = fmaf(r[0], xs, r[1]);
+                bdx = fmaf(r[2], xs, r[3]);
+                dy01 = ys01; dy23 = ys23;                          // w = c y + (b x + gamma)
+            } else {
+                dx = xs - r[0];
+                dy01 = __fadd2_rn(ys01, make_float2(-r[1], -r[1]));
+                dy23 = __fadd2_rn(ys23, make_float2(-r[1], -r[1]));
+                u = r[2] * dx;
+                bdx = r[3] * dx;
+            }
+            const float uu = u * u;
             const float2 w01 = __ffma2_rn(make_float2(r[4], r[4]), dy01, make_float2(bdx, bdx));
             const float2 w23 = __ffma2_rn(make_float2(r[4], r[4]), dy23, make_float2(bdx, bdx));
             const float2 q01 = __ffma2_rn(w01, w01, make_float2(uu, uu));

@@ -233,7 +233,7 @@ RENDER_CASES = [
 
 
 @pytest.mark.parametrize("H,W,C,K,order,scale", RENDER_CASES)
-def test_render_parity(H, W, C, K, order, scale):
+def test_render_parity(H, W, C, K, order, scale, monkeypatch):
     oH, oW = int(round(H * scale)), int(round(W * scale))
     pool = synth.aniso_pool(H, W, C, K, 10 + K, order=order, margin_px=6, log_pi_sd=0.5)
     pool = conditioned(pool, H, W, oH, oW)
@@ -242,12 +242,19 @@ def test_render_parity(H, W, C, K, order, scale):
     y_ref, D_ref = O.render(opar(pool), H, W, oH, oW)
     assert (D_ref > 0).mean() > 0.5
     assert_pixels(y, y_ref)
-    # deterministic: the forward has no atomics; the float4 store epilogue
-    # writes the same pixels (ragged widths fall back to scalar stores)
+    # deterministic: the forward has no atomics
+    np.testing.assert_array_equal(y, h.render(dev_pool(pool), oH, oW).cpu().numpy())
+    # the float4 store epilogue of the two-pixel form writes the same pixels
+    # as its scalar one (ragged widths fall back to scalar stores); the
+    # four-pixel form (the default on short buckets) evaluates the cull test
+    # on block-centred records, so it agrees with the two-pixel form to
+    # rounding, and both meet the oracle bar
+    monkeypatch.setenv("SMOE_RENDER4", "0")
     y2 = h.render(dev_pool(pool), oH, oW).cpu().numpy()
-    np.testing.assert_array_equal(y, y2)
     y4 = h.render(dev_pool(pool), oH, oW, vector_stores=True).cpu().numpy()
-    np.testing.assert_array_equal(y, y4)
+    np.testing.assert_array_equal(y2, y4)
+    assert_pixels(y2, y_ref)
+    np.testing.assert_allclose(y2, y, rtol=2e-6, atol=1e-7)
     acc = torch.full((C, oH, oW), 0.25, device="cuda")
     h.render(dev_pool(pool), oH, oW, out=acc, accumulate=0.5, vector_stores=True)
     np.testing.assert_allclose(acc.cpu().numpy(), 0.25 + 0.5 * y, rtol=1e-6, atol=1e-7)
