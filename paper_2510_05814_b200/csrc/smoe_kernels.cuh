@@ -1329,8 +1329,16 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
     const int px = tx * TILE + (warp & 1) * 8 + (lane & 7);
     const int py0 = ty * TILE + (warp >> 1) * 8 + (lane >> 3) * 2, py1 = py0 + 1;
     const bool v0 = px < A.oW && py0 < A.oH, v1 = px < A.oW && py1 < A.oH;
-    const float xs = (px + 0.5f) * A.sx - 0.5f;
-    const float ys0 = (py0 + 0.5f) * A.sy - 0.5f, ys1 = (py1 + 0.5f) * A.sy - 0.5f;
+    // XF (render, constant experts; SMOE_R4_XF): the block-centred records
+    // of k_render4 -- coordinates relative to the block's first sample, the
+    // staged record's first float4 rewritten to {a, -a mx, b, -(b mx + c my)}
+    // -- so the cull test is FFMA, FFMA, FFMA2 + FMUL, FFMA2.  (The train
+    // raster measured slower with it: DESIGN.md §10.)
+    constexpr bool XF = SMOE_R4_XF && !TRAIN && E == 1 && C == 3;   // (C = 1 spills at the 40-register bound)
+    const float X0 = XF ? (tx * TILE + 0.5f) * A.sx - 0.5f : 0.f;
+    const float Y0 = XF ? (ty * TILE + 0.5f) * A.sy - 0.5f : 0.f;
+    const float xs = (px + 0.5f) * A.sx - 0.5f - X0;
+    const float ys0 = (py0 + 0.5f) * A.sy - 0.5f - Y0, ys1 = (py1 + 0.5f) * A.sy - 0.5f - Y0;
     const float R2 = A.R2;
     const int s0 = A.len ? tile * A.bcap : A.start[tile];
     const int n = A.len ? A.len[tile] : A.start[tile + 1] - s0;
@@ -1372,6 +1380,15 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
             if (TRAIN && q == 0) sid[j] = id;
         }
         __syncthreads();
+        if (XF) {
+            for (int j = threadIdx.x; j < nb; j += blockDim.x) {
+                const float4 f0 = srec[j * RS4];
+                const float c = srec[j * RS4 + 1].x;
+                const float mx = f0.x - X0, my = f0.y - Y0;
+                srec[j * RS4] = make_float4(f0.z, -f0.z * mx, f0.w, -fmaf(f0.w, mx, c * my));
+            }
+            __syncthreads();
+        }
     };
     auto load_rec = [&](int j, float (&r)[R::RS]) {
 #pragma unroll
@@ -1385,11 +1402,19 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
     // done pairwise with packed f32x2 instructions (FADD2/FMUL2/FFMA2, sm_100).
     const float2 ys2 = make_float2(ys0, ys1);
     auto dist2 = [&](const float (&r)[R::RS], float &dx, float2 &dy, float &u, float2 &w, float2 &q) {
-        dx = xs - r[0];
-        dy = __fadd2_rn(ys2, make_float2(-r[1], -r[1]));
-        u = r[2] * dx;
-        const float bdx = r[3] * dx;
-        w = __ffma2_rn(make_float2(r[4], r[4]), dy, make_float2(bdx, bdx));
+        if (XF) {   // dx, dy unused (constant experts, no backward)
+            dx = 0.f;
+            dy = make_float2(0.f, 0.f);
+            u = fmaf(r[0], xs, r[1]);
+            const float bx = fmaf(r[2], xs, r[3]);
+            w = __ffma2_rn(make_float2(r[4], r[4]), ys2, make_float2(bx, bx));
+        } else {
+            dx = xs - r[0];
+            dy = __fadd2_rn(ys2, make_float2(-r[1], -r[1]));
+            u = r[2] * dx;
+            const float bdx = r[3] * dx;
+            w = __ffma2_rn(make_float2(r[4], r[4]), dy, make_float2(bdx, bdx));
+        }
         const float uu = u * u;
         q = __ffma2_rn(w, w, make_float2(uu, uu));
     };
