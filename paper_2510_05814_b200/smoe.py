@@ -336,6 +336,12 @@ class SMoE:
                     _check(lib().smoe_render_ex(*args), self.h)
         return out
 
+    def invalidate(self):
+        """smoe_invalidate: the caller wrote the parameter buffers outside the
+        tensors' version counters (e.g. through ``.data`` or raw pointers);
+        the next step re-derives the kernel records."""
+        _check(lib().smoe_invalidate(self.h), self.h)
+
     def set_band(self, tile_row0: int, tile_row1: int):
         _check(lib().smoe_set_band(self.h, tile_row0, tile_row1), self.h)
 

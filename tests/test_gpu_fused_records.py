@@ -131,3 +131,34 @@ def test_fused_emission_overflow_recovers(monkeypatch, binning):
     np.testing.assert_allclose(lb, la, rtol=1e-4)
     for x, y in zip(pa, pb):
         np.testing.assert_allclose(y, x, rtol=1e-3, atol=1e-4)
+
+
+def test_explicit_invalidate_after_untracked_write(monkeypatch):
+    """A write the binding cannot see (through ``.data``, which does not move
+    the tensor's version counter) followed by ``smoe_invalidate``: the next
+    gradient pass bins afresh (cold launch count) and equals a new handle's."""
+    perm, warm, cold = BINNINGS["two_stage"]
+    monkeypatch.setenv("SMOE_PERM", perm)
+    monkeypatch.setenv("SMOE_FUSE_REC", "1")
+    C, order = 3, 0
+    pool = synth.aniso_pool(H, W, C, K, 3, order=order)
+    prm = smoe.Params.from_numpy(pool, "cuda:0")
+    tgt = torch.as_tensor(synth.image(H, W, C, 4)).cuda()
+    h = smoe.SMoE(K, H, W, C, order)
+    for it in range(5):
+        h.step(prm, tgt, smoe.LR(), stats=(it == 0))
+    torch.cuda.synchronize()
+    v0 = prm.mu._version
+    prm.mu.data.add_(0.37)
+    assert prm.mu._version == v0                      # invisible to the binding
+    h.invalidate()
+    n0 = h.launch_count()
+    g1, s1 = _grad(h, prm, tgt)
+    assert h.launch_count() - n0 == cold
+    h2 = smoe.SMoE(K, H, W, C, order)
+    g2, s2 = _grad(h2, prm.clone(), tgt)
+    h.close()
+    h2.close()
+    np.testing.assert_allclose(s1[:3], s2[:3], rtol=1e-12, atol=0)
+    tol = 1e-5 * np.abs(g2) + 1e-6 * np.abs(g2).max()
+    assert not (np.abs(g1 - g2) > tol).any()
