@@ -64,6 +64,11 @@ constexpr int TILE = 16;                 // 16x16 blocks
     do {              \
     } while (0)
 #endif
+#ifndef SMOE_SEED_SOA
+#define SMOE_SEED_SOA 1                  // backward seeds as 32-bit SoA: conflict-free loads of random pixel slots
+                                         // (config 3 raster 264.5 -> 259.1 us, config 2 48.6 -> 47.0 us; the
+                                         // 16-byte slot layout carried 85% of the raster's bank-conflict wavefronts)
+#endif
 #ifndef SMOE_R4_XF
 #define SMOE_R4_XF 1                     // four-pixel render: cull test on block-centred records (constant experts)
 #endif
@@ -1593,6 +1598,19 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
         }
         if (lane == 0) { red[0][warp] = (double)sse; red[1][warp] = (double)ssec; red[2][warp] = (double)unc; }
         if (MASKS) {
+            if (SMOE_SEED_SOA) {
+                // one float per (component, thread): component k of thread t at
+                // [k * 128 + t] -- the backward's 32-bit loads of random pixel
+                // slots hit 32 distinct banks (no conflicts; more loads)
+                float *sf = reinterpret_cast<float *>(spix) + threadIdx.x;
+                if (C == 1) {
+                    sf[0] = eD0[0]; sf[128] = eD1[0]; sf[256] = K0; sf[384] = K1; sf[512] = xs; sf[640] = ys0;
+                } else {
+#pragma unroll
+                    for (int c = 0; c < C; c++) { sf[256 * c] = eD0[c]; sf[256 * c + 128] = eD1[c]; }
+                    sf[256 * C] = K0; sf[256 * C + 128] = K1; sf[256 * C + 256] = xs; sf[256 * C + 384] = ys0;
+                }
+            } else {
             float4 *sp = spix + NSEED * threadIdx.x;
             if (C == 1) {
                 sp[0] = make_float4(eD0[0], eD1[0], K0, K1);
@@ -1601,6 +1619,7 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
                 sp[0] = make_float4(eD0[0], eD1[0], eD0[C > 1 ? 1 : 0], eD1[C > 1 ? 1 : 0]);
                 sp[1] = make_float4(eD0[C > 2 ? 2 : 0], eD1[C > 2 ? 2 : 0], K0, K1);
                 sp[2] = make_float4(xs, ys0, 0.f, 0.f);
+            }
             }
         }
         __syncthreads();
@@ -1676,7 +1695,8 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
     // entries; a lane accumulates the raw sums of the current kernel in
     // registers and flushes them with vector atomics when the kernel changes
     // and at the end of its range.
-    const float4 *spw_pix = spix + warp * 32 * NSEED;   // this warp's lanes' seeds
+    const float4 *spw_pix = SMOE_SEED_SOA ? reinterpret_cast<const float4 *>(reinterpret_cast<const float *>(spix) + warp * 32)
+                                          : spix + warp * 32 * NSEED;   // this warp's lanes' seeds
     unsigned spw_pix_s = (unsigned)__cvta_generic_to_shared(spw_pix);
     unsigned srec_s = (unsigned)__cvta_generic_to_shared(srec), sid_s = (unsigned)__cvta_generic_to_shared(sid);
     if (E == 3) {
@@ -1780,14 +1800,23 @@ __device__ __forceinline__ void raster_tile(const RasterArgs &A, const int tile)
                 const int l = 31 - __clz(lb);
                 const bool h0 = (kr.x & lb) != 0u, h1 = (kr.y & lb) != 0u;
                 // this pair's seeds and coordinates (a pixel outside the ellipse: g = 0)
-                const unsigned a = spw_pix_s + (unsigned)l * (16u * NSEED);
                 float2 ed[C], Kp, xy;
-                if (C == 1) {
+                if (SMOE_SEED_SOA) {
+                    // spw_pix_s = the warp's column (warp * 32 floats); component k at + 512 k bytes
+                    const unsigned a = spw_pix_s + 4u * (unsigned)l;
+                    auto ld = [&](unsigned off) { return __int_as_float(lds32(a + off)); };
+#pragma unroll
+                    for (int c = 0; c < C; c++) ed[c] = make_float2(ld(1024u * c), ld(1024u * c + 512u));
+                    Kp = make_float2(ld(1024u * C), ld(1024u * C + 512u));
+                    xy = make_float2(ld(1024u * C + 1024u), ld(1024u * C + 1536u));
+                } else if (C == 1) {
+                    const unsigned a = spw_pix_s + (unsigned)l * (16u * NSEED);
                     const float4 p0 = lds128(a), p1 = lds128(a + 16u);
                     ed[0] = make_float2(p0.x, p0.y);
                     Kp = make_float2(p0.z, p0.w);
                     xy = make_float2(p1.x, p1.y);
                 } else {
+                    const unsigned a = spw_pix_s + (unsigned)l * (16u * NSEED);
                     const float4 p0 = lds128(a), p1 = lds128(a + 16u);
                     const float2 p2 = lds64(a + 32u);
                     ed[0] = make_float2(p0.x, p0.y);
